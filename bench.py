@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the batched 2x2 SVD hot path on B200 (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3], the largest single-GPU config): real
+fp64, n = 2^30 matrices, SoA trains, entries +-U[1,2)*2^e with e uniform in
+[-100, 100], seeded counter-based synthetic data generated on each GPU for
+its own contiguous shard (strong scaling: the total n is fixed, sharded over
+N GPUs with no collective on the data path).  One step = one pass of the
+fused kernel over the shard, inputs already resident in HBM (34 GB of inputs
+per step on one GPU: larger than L2, so no flush is needed).  Config 4
+(complex, n = 2^28, mixed structure) is measured the same way and reported
+under "complex".
+
+"e2e": the same metric through the reference-facing host-buffer C-ABI
+(b2s_svd2_real_host via run_batch_into) with pinned host trains: every step
+copies that step's inputs host->device and all outputs device->host.
+
+"cpu_baseline" / --impl reference: the CPU oracle (a C port of the
+reference pipeline; the reference itself is Python and not installable on
+the GPU box) on all host threads, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = ("2x2 SVDs/sec (fp64, real & complex) and % of HBM/FP64 roofline "
+          "at 1/2/4/8 B200")
+UNIT = "SVD/s"
+BYTES_PER_SVD = {"real": 120, "complex": 216}     # in + out trains
+FLOPS_PER_SVD = {"real": 70, "complex": 178}
+SEED = 20250705
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+def ncu_traffic(config):
+    """Per-launch DRAM bytes from the committed ncu --set full summary."""
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get(str(config))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.fh = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.fh.flush()
+        with open(self.fh.name) as fh:
+            rows = [r.strip().split(", ") for r in fh if r.strip()]
+        os.unlink(self.fh.name)
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+                power.append(float(r[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_sample_rate(config, budget_s=12.0, sample=1 << 22, threads=None):
+    """Oracle throughput on host cores over a bounded sample of the workload."""
+    import oracle
+    from paper_2005_07403_b200 import synth
+    threads = threads or os.cpu_count() or 1
+    re, im = synth.generate(config, SEED, 0, sample)
+    oracle.svd2(re[:, :4096], None if im is None else im[:, :4096], threads=threads)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.svd2(re, im, threads=threads)
+        done += sample
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return done / el, threads, done
+
+
+def run_device(config, world, rank, local, steps, warmup):
+    """Device-resident throughput of the fused kernel on this rank's shard."""
+    import torch
+    import paper_2005_07403_b200 as b2s
+    from paper_2005_07403_b200 import synth
+    from paper_2005_07403_b200.svd2 import launch_device
+    cfg = synth.CONFIGS[config]
+    field = cfg["field"]
+    n_total = cfg["n"]
+    lo, hi = b2s.shards(n_total, world)[rank]
+    n = hi - lo
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    b2s.assert_device_fp_env(local)
+    re, im = synth.generate_device(config, SEED, lo, n, device=dev)
+    out = b2s.SvdBatchOut.empty(n, im is not None, device=dev)
+    outd = {"u_re": [out.u_re[t] for t in range(4)],
+            "u_im": None if im is None else [out.u_im[t] for t in range(4)],
+            "v_re": [out.v_re[t] for t in range(4)],
+            "v_im": None if im is None else [out.v_im[t] for t in range(4)],
+            "smax": out.smax, "smin": out.smin, "shift": out.shift}
+    in_re = [re[t] for t in range(4)]
+    in_im = None if im is None else [im[t] for t in range(4)]
+    stream = torch.cuda.current_stream(dev)
+    step = lambda: launch_device(n, in_re, in_im, outd, 0, 0, None, stream.cuda_stream)
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local) if rank == 0 else None
+    time.sleep(0.3 if clocks else 0.0)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(steps):
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clk = clocks.stop() if clocks else None
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = max_over_ranks(total_ms, world)
+    avg_kernel_ms = max_over_ranks(float(np.mean(kern_ms)), world)
+    del re, im, out, outd, in_re, in_im
+    torch.cuda.empty_cache()
+    return {"n_total": n_total, "n_shard": n, "field": field,
+            "total_ms": total_ms, "avg_kernel_ms": avg_kernel_ms,
+            "clocks": clk, "launches": steps}
+
+
+def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
+    """Same metric through the host-buffer C-ABI with pinned host trains."""
+    import torch
+    import paper_2005_07403_b200 as b2s
+    from paper_2005_07403_b200 import synth
+    cfg = synth.CONFIGS[config]
+    n_total = cfg["n"]
+    lo, hi = b2s.shards(n_total, world)[rank]
+    n = min(hi - lo, max_lanes)
+    n -= n % 8
+    cplx = cfg["field"] == "complex"
+    pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    # inputs: generated on the device, parked in pinned host memory
+    dre, dim = synth.generate_device(config, SEED, lo, n, device=torch.device("cuda", local))
+    re = pin((4, n))
+    re[:] = dre.cpu().numpy()
+    im = None
+    if cplx:
+        im = pin((4, n))
+        im[:] = dim.cpu().numpy()
+    del dre, dim
+    batch = b2s.Batch2x2(n=n, re=re, im=im)
+    out = b2s.SvdBatchOut(n=n, u_re=pin((4, n)), u_im=pin((4, n)) if cplx else None,
+                          v_re=pin((4, n)), v_im=pin((4, n)) if cplx else None,
+                          smax=pin((n,)), smin=pin((n,)), shift=pin((n,)))
+    rc = b2s.RunConfig(field=cfg["field"], devices=(local,))
+    for _ in range(warmup):
+        b2s.run_batch_into(batch, out, rc)
+    barrier(world)
+    walls = []
+    for _ in range(steps):
+        walls.append(b2s.run_batch_into(batch, out, rc))
+    barrier(world)
+    t = max_over_ranks(float(np.mean(walls)), world)
+    n_all = n * world
+    nin = 8 if cplx else 4
+    nout = 19 if cplx else 11
+    return {"value": n_all / t, "unit": UNIT, "lanes_per_step": n_all,
+            "h2d_bytes_per_step": n_all * nin * 8, "d2h_bytes_per_step": n_all * nout * 8,
+            "ms_per_step": t * 1e3, "path": "run_batch_into -> b2s_svd2_%s_host (pinned)"
+            % cfg["field"]}
+
+
+def roofline(res, config, hbm, how):
+    field = res["field"]
+    bytes_per_launch = BYTES_PER_SVD[field] * res["n_shard"]
+    achieved = bytes_per_launch / (res["avg_kernel_ms"] * 1e-3) / 1e9
+    traffic = ncu_traffic(config)
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+            "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_source": how,
+            "traffic": traffic,
+            "algorithmic_bytes_per_launch": bytes_per_launch,
+            "fp64_tflops": round(FLOPS_PER_SVD[field] * res["n_shard"]
+                                 / (res["avg_kernel_ms"] * 1e-3) / 1e12, 3)}
+
+
+def main_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2005_07403_b200 import synth
+    config = args.config
+    sample = 1 << 22
+    re, im = synth.generate(config, SEED, 0, sample)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.svd2(re, im, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.svd2(re, im, threads=threads)
+    el = time.perf_counter() - t0
+    v = sample * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(config, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": "first 2^22 lanes of config %d per step "
+                                       "(oracle/svd2_oracle.c, C port of lanesvd "
+                                       "svd2_lanes; reference is Python, not "
+                                       "installable on the GPU box)" % config},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(config, world):
+    from paper_2005_07403_b200 import synth
+    c = synth.CONFIGS[config]
+    desc = {3: "config3: real fp64 2x2 SVD, n=2^30, e in [-100,100], SoA trains",
+            4: "config4: complex fp64 2x2 SVD, n=2^28, mixed structure, SoA trains"}
+    return {"workload": desc.get(config, "config%d" % config), "n": c["n"],
+            "field": c["field"], "parallelism": "shard%d (contiguous lane ranges, no collective)" % world,
+            "l2": "inputs larger than L2 (no flush needed)", "seed": SEED}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-complex", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-lanes", type=int, default=1 << 27)
+    args = ap.parse_args()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        return main_reference(args, world, rank)
+    hbm, how = peaks()
+    res = run_device(args.config, world, rank, local, args.steps, args.warmup)
+    value = res["n_total"] * args.steps / (res["total_ms"] * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args.config, world),
+            "roofline": roofline(res, args.config, hbm, how),
+            "gpu_launches": res["launches"], "clocks": res["clocks"]}
+    if not args.no_complex and args.config == 3:
+        cres = run_device(4, world, rank, local, args.steps, args.warmup)
+        line["complex"] = {
+            "value": cres["n_total"] * args.steps / (cres["total_ms"] * 1e-3),
+            "unit": UNIT, "ms_per_step": cres["total_ms"] / args.steps,
+            "config": workload_config(4, world),
+            "roofline": roofline(cres, 4, hbm, how), "clocks": cres["clocks"]}
+        line["gpu_launches"] += cres["launches"]
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(args.config, world, rank, local,
+                              max(1, min(args.steps, 5)), 1, args.e2e_lanes)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, done = cpu_sample_rate(args.config)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": "%d lanes of config %d (repeated 2^22-lane "
+                                          "prefix, ~12 s) through oracle/svd2_oracle.c "
+                                          "on %d threads" % (done, args.config, cores)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,126 @@
+/*
+ * b2s.h -- C ABI of the B200-native batched 2x2 SVD engine (libb2s.so).
+ *
+ * Drop-in boundary for the reference's batched SVD path (lanesvd 0.1.0):
+ * every entry point below replaces one Python-level seam of the reference and
+ * keeps its structure-of-arrays layout, its argument meaning and its error
+ * classes.  Plain pointers and sizes only; no torch types.
+ *
+ * Layout (layout.py:1-16, 69-130): a batch of n matrices is a set of "trains",
+ * one contiguous float64 array per matrix entry in column-major entry order
+ * (e11, e21, e12, e22); lane k of every train belongs to matrix k.  Complex
+ * batches pass separate real and imaginary trains.  Outputs: U and V trains
+ * in the same order, smax/smin (scaled singular values) and shift (the
+ * power-of-two exponent s, DBL_MAX for a zero matrix, -0.0 once backscaled).
+ *
+ * Return codes: 0 success; >0 invalid argument (Python layer raises
+ * ValueError, as the reference does); <0 CUDA error (RuntimeError).
+ * b2s_last_error() gives a thread-local message for the last failure.
+ *
+ * Device entry points are asynchronous on the given stream (cudaStream_t
+ * passed as void*; NULL = legacy default stream) and perform no allocation.
+ * All are reentrant; call them from one host thread per GPU.
+ */
+#ifndef B2S_H
+#define B2S_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* backscale modes, driver.py:34 BACKSCALE_MODES / svd2.py:481-514 */
+#define B2S_BACKSCALE_NONE 0
+#define B2S_BACKSCALE_SAFE 1
+#define B2S_BACKSCALE_UNCONDITIONAL 2
+
+/* flags */
+#define B2S_FLAG_SINE_FORM 1   /* svd2_lanes(sine_form=True), svd2.py:427-474 */
+#define B2S_FLAG_STATES 2      /* also write the _dump_states trains, driver.py:193-216 */
+
+/* Number of state trains written with B2S_FLAG_STATES (driver.py:193-216). */
+#define B2S_STATES_REAL 16
+#define B2S_STATES_COMPLEX 20
+
+/* ABI version (major*100 + minor). */
+int b2s_version(void);
+
+/* Thread-local description of the last non-zero return. */
+const char *b2s_last_error(void);
+
+/*
+ * Real batch on the device.  Replaces the per-slab seam
+ * driver._run_lanes(parts, out, lo, hi, sine_form, backscale_mode)
+ * (driver.py:73-85) = svd2.svd2_lanes (svd2.py:521-570) + svd2.backscale
+ * (svd2.py:481-514) + the stores into out[lo:hi].
+ *   a[4]      device pointers to the input trains e11, e21, e12, e22
+ *   u[4],v[4] device pointers to the output trains u11, u21, u12, u22 / v..
+ *   smax, smin, shift   device pointers, n doubles each
+ *   states    NULL, or B2S_STATES_REAL device train pointers (needs
+ *             B2S_FLAG_STATES)
+ * Every pointer must be 8-byte aligned (the trains of aligned_zeros / torch
+ *            storage are 64-byte aligned, which the kernels exploit).
+ */
+int b2s_svd2_real(int64_t n, const double *const a[4], double *const u[4],
+                  double *const v[4], double *smax, double *smin,
+                  double *shift, int backscale_mode, int flags,
+                  double *const *states, void *stream);
+
+/* Complex batch on the device; same seam, 8-train path (`im is not None`). */
+int b2s_svd2_complex(int64_t n, const double *const a_re[4],
+                     const double *const a_im[4], double *const u_re[4],
+                     double *const u_im[4], double *const v_re[4],
+                     double *const v_im[4], double *smax, double *smin,
+                     double *shift, int backscale_mode, int flags,
+                     double *const *states, void *stream);
+
+/*
+ * Host-buffer variants: the reference-facing call a ctypes/cffi binding of
+ * driver.run_batch (driver.py:149-190) makes with numpy trains.  Inputs and
+ * outputs are HOST pointers (pinned memory gives full PCIe overlap); the
+ * batch is streamed through `device` in chunks of `chunk` lanes (0 = auto)
+ * with copy-in, kernel and copy-out overlapped on three streams.  Blocking;
+ * returns after every output byte is back in host memory.
+ */
+int b2s_svd2_real_host(int64_t n, const double *const a[4], double *const u[4],
+                       double *const v[4], double *smax, double *smin,
+                       double *shift, int backscale_mode, int flags,
+                       int device, int64_t chunk);
+
+int b2s_svd2_complex_host(int64_t n, const double *const a_re[4],
+                          const double *const a_im[4], double *const u_re[4],
+                          double *const u_im[4], double *const v_re[4],
+                          double *const v_im[4], double *smax, double *smin,
+                          double *shift, int backscale_mode, int flags,
+                          int device, int64_t chunk);
+
+/*
+ * Standalone device backscale: svd2.backscale(smax, smin, shift, mode)
+ * (svd2.py:481-514), out-of-place (outputs may alias inputs).
+ */
+int b2s_backscale(int64_t n, const double *smax, const double *smin,
+                  const double *shift, int backscale_mode, double *out_smax,
+                  double *out_smin, double *out_shift, void *stream);
+
+/*
+ * Seeded synthetic batches of the BASELINE configs 0-4 (counter-based, so
+ * any lane range regenerates bit-identically on host and device).  Writes
+ * lanes [lane0, lane0 + n) of config `config` into re[4] (and im[4] for the
+ * complex configs 1 and 4; pass NULLs for real configs).
+ */
+int b2s_synth(int config, uint64_t seed, int64_t lane0, int64_t n,
+              double *const re[4], double *const im[4], void *stream);
+
+/*
+ * Device floating-point environment canary, the GPU analogue of
+ * lanes.assert_fp_env (lanes.py:274-302): round-to-nearest-even, gradual
+ * underflow and a fused fma on `device`.  Blocking.  0 = environment OK.
+ */
+int b2s_check_fp_env(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B2S_H */

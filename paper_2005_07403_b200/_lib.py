@@ -1,0 +1,95 @@
+"""ctypes binding of the native engine ``_native/libb2s.so`` (include/b2s.h).
+
+The CUDA library is the only compute path: if it is missing this module
+raises at import, there is no CPU fallback.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or
+``python -m paper_2005_07403_b200.build``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_native", "libb2s.so")
+
+BACKSCALE = {"none": 0, "safe": 1, "unconditional": 2}
+FLAG_SINE_FORM = 1
+FLAG_STATES = 2
+STATES_REAL = 16
+STATES_COMPLEX = 20
+
+# exported symbols, exactly the functions declared in include/b2s.h
+SYMBOLS = (
+    "b2s_version", "b2s_last_error", "b2s_svd2_real", "b2s_svd2_complex",
+    "b2s_svd2_real_host", "b2s_svd2_complex_host", "b2s_backscale",
+    "b2s_synth", "b2s_check_fp_env",
+)
+
+_P = ctypes.c_void_p
+_PA = ctypes.POINTER(ctypes.c_void_p)   # array of train pointers
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+
+
+class NativeLibraryMissing(ImportError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            "libb2s.so not built (%s); run __graft_entry__.build()" % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    L.b2s_version.restype = _int
+    L.b2s_last_error.restype = ctypes.c_char_p
+    L.b2s_svd2_real.argtypes = [_i64, _PA, _PA, _PA, _P, _P, _P, _int, _int,
+                                _PA, _P]
+    L.b2s_svd2_complex.argtypes = [_i64, _PA, _PA, _PA, _PA, _PA, _PA, _P, _P,
+                                   _P, _int, _int, _PA, _P]
+    L.b2s_svd2_real_host.argtypes = [_i64, _PA, _PA, _PA, _P, _P, _P, _int,
+                                     _int, _int, _i64]
+    L.b2s_svd2_complex_host.argtypes = [_i64, _PA, _PA, _PA, _PA, _PA, _PA,
+                                        _P, _P, _P, _int, _int, _int, _i64]
+    L.b2s_backscale.argtypes = [_i64, _P, _P, _P, _int, _P, _P, _P, _P]
+    L.b2s_synth.argtypes = [_int, ctypes.c_uint64, _i64, _i64, _PA, _PA, _P]
+    L.b2s_check_fp_env.argtypes = [_int]
+    for name in SYMBOLS:
+        if name not in ("b2s_version", "b2s_last_error"):
+            getattr(L, name).restype = _int
+    return L
+
+
+lib = _load()
+
+
+def ptr_array(ptrs):
+    """A C array of raw addresses (ints)."""
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    return ctypes.cast(arr, _PA), arr
+
+
+def check(rc, what):
+    """Map a C-ABI return code onto the reference's exception classes."""
+    if rc == 0:
+        return
+    msg = "%s: %s" % (what, lib.b2s_last_error().decode(errors="replace"))
+    if rc > 0:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+_env_checked = set()
+_env_lock = threading.Lock()
+
+
+def assert_device_fp_env(device):
+    """GPU analogue of lanes.assert_fp_env (lanes.py:274-302), once per
+    device: round-to-nearest-even, gradual underflow, fused fma."""
+    with _env_lock:
+        if device in _env_checked:
+            return
+        check(lib.b2s_check_fp_env(int(device)), "device FP environment")
+        _env_checked.add(device)

@@ -1,0 +1,180 @@
+"""Lane-level entry points of the GPU pipeline (drop-in for lanesvd.svd2).
+
+``svd2_lanes`` and ``backscale`` keep the reference signatures
+(svd2.py:521-570, 481-514) but run the fused sm_100a kernels through the
+C-ABI.  Trains may be host NumPy arrays (staged through HBM and returned as
+NumPy) or CUDA tensors (processed in place on their device, results left in
+HBM).  The per-phase helpers of the reference (compute_scale ... assemble_uv)
+have no separate kernels: all phases are fused in registers; their
+intermediate values are exported by ``with_states=True`` instead.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .layout import is_device_array
+
+__all__ = ["HEADROOM_EXP", "SQRT_DBL_MAX", "Svd2", "LaneStates",
+           "svd2_lanes", "backscale", "launch_device"]
+
+HEADROOM_EXP = 1021.0                  # svd2.py:52-56
+SQRT_DBL_MAX = 1.34078079299425956e+154  # svd2.py:58-59
+
+# driver.py:193-216 state-train order
+STATE_NAMES_REAL = ("shift", "swap_cols", "swap_rows", "row_phase1",
+                    "row_phase2", "r12_phase", "r22_phase", "givens_tan",
+                    "givens_cos", "r11", "r12", "r22", "left_tan",
+                    "right_tan", "smax_scaled", "smin_scaled")
+STATE_NAMES_COMPLEX = ("shift", "swap_cols", "swap_rows",
+                       "row_phase1_re", "row_phase1_im",
+                       "row_phase2_re", "row_phase2_im",
+                       "r12_phase_re", "r12_phase_im",
+                       "r22_phase_re", "r22_phase_im", "givens_tan",
+                       "givens_cos", "r11", "r12", "r22", "left_tan",
+                       "right_tan", "smax_scaled", "smin_scaled")
+
+
+@dataclass
+class Svd2:
+    """Assembled factors (svd2.py:108-127): U/V entries as (re, im) pairs in
+    column-major entry order (im None for real lanes), scaled singular
+    values and the shift."""
+    u11: tuple
+    u21: tuple
+    u12: tuple
+    u22: tuple
+    v11: tuple
+    v21: tuple
+    v12: tuple
+    v22: tuple
+    smax_scaled: object
+    smin_scaled: object
+    shift: object
+
+
+class LaneStates(dict):
+    """Intermediate per-lane quantities of the fused kernel, keyed by the
+    names of driver._dump_states' train order."""
+
+    def trains(self):
+        return list(self.values())
+
+
+def _stream_of(t):
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _addr(t):
+    return t.data_ptr()
+
+
+def launch_device(n, in_re, in_im, out, mode, flags=0, states=None,
+                  stream=None):
+    """Run the device C-ABI on CUDA tensors.
+
+    in_re/in_im: sequences of 4 device trains (in_im None for real);
+    out: dict with u_re, u_im, v_re, v_im (sequences of 4 trains) and smax,
+    smin, shift trains; states: sequence of state trains or None.  Launches
+    asynchronously on ``stream`` (default: torch's current stream)."""
+    if stream is None:
+        stream = _stream_of(in_re[0])
+    a, _k1 = _lib.ptr_array([_addr(x) for x in in_re])
+    u, _k2 = _lib.ptr_array([_addr(x) for x in out["u_re"]])
+    v, _k3 = _lib.ptr_array([_addr(x) for x in out["v_re"]])
+    st, _k4 = (None, None)
+    if states is not None:
+        st, _k4 = _lib.ptr_array([_addr(x) for x in states])
+        flags |= _lib.FLAG_STATES
+    if in_im is None:
+        rc = _lib.lib.b2s_svd2_real(
+            int(n), a, u, v, _addr(out["smax"]), _addr(out["smin"]),
+            _addr(out["shift"]), mode, flags, st, stream)
+        _lib.check(rc, "b2s_svd2_real")
+        return
+    ai, _k5 = _lib.ptr_array([_addr(x) for x in in_im])
+    ui, _k6 = _lib.ptr_array([_addr(x) for x in out["u_im"]])
+    vi, _k7 = _lib.ptr_array([_addr(x) for x in out["v_im"]])
+    rc = _lib.lib.b2s_svd2_complex(
+        int(n), a, ai, u, ui, v, vi, _addr(out["smax"]), _addr(out["smin"]),
+        _addr(out["shift"]), mode, flags, st, stream)
+    _lib.check(rc, "b2s_svd2_complex")
+
+
+def _to_device(x, device):
+    import torch
+    if is_device_array(x):
+        return x.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(device)
+
+
+def svd2_lanes(parts, sine_form=False, with_states=False, device=None):
+    """Full pipeline on component trains (svd2.py:521-570).
+
+    parts: 4 trains (e11, e21, e12, e22) for real lanes or 8 with re/im
+    interleaved per entry.  Returns ``Svd2`` (and ``LaneStates`` when
+    ``with_states``); host inputs give host results."""
+    import torch
+    if len(parts) not in (4, 8):
+        raise ValueError("expected 4 or 8 component trains, got %d"
+                         % len(parts))
+    host = not is_device_array(parts[0])
+    if device is None:
+        device = parts[0].device if not host else torch.device(
+            "cuda", torch.cuda.current_device())
+    dev_parts = [_to_device(p, device) for p in parts]
+    n = int(dev_parts[0].shape[0])
+    for p in dev_parts:
+        if p.shape != (n,):
+            raise ValueError("component trains must be equal-length vectors")
+    _lib.assert_device_fp_env(torch.device(device).index or 0)
+    cplx = len(parts) == 8
+    in_re = dev_parts[0::2] if cplx else dev_parts
+    in_im = dev_parts[1::2] if cplx else None
+    E = lambda: torch.empty(n, dtype=torch.float64, device=device)
+    out = {"u_re": [E() for _ in range(4)], "v_re": [E() for _ in range(4)],
+           "u_im": [E() for _ in range(4)] if cplx else None,
+           "v_im": [E() for _ in range(4)] if cplx else None,
+           "smax": E(), "smin": E(), "shift": E()}
+    names = STATE_NAMES_COMPLEX if cplx else STATE_NAMES_REAL
+    states = [E() for _ in names] if with_states else None
+    launch_device(n, in_re, in_im, out, 0,
+                  _lib.FLAG_SINE_FORM if sine_form else 0, states)
+    fin = (lambda t: t.cpu().numpy()) if host else (lambda t: t)
+    pair = lambda k: (fin(out["u_re"][k]), fin(out["u_im"][k]) if cplx else None)
+    vpair = lambda k: (fin(out["v_re"][k]), fin(out["v_im"][k]) if cplx else None)
+    svd = Svd2(u11=pair(0), u21=pair(1), u12=pair(2), u22=pair(3),
+               v11=vpair(0), v21=vpair(1), v12=vpair(2), v22=vpair(3),
+               smax_scaled=fin(out["smax"]), smin_scaled=fin(out["smin"]),
+               shift=fin(out["shift"]))
+    if with_states:
+        return svd, LaneStates(zip(names, [fin(s) for s in states]))
+    return svd
+
+
+def backscale(smax_scaled, smin_scaled, shift, mode="safe"):
+    """Divide the shift back out of the singular values (svd2.py:481-514),
+    on the GPU.  Lanes rescaled get shift -0.0; "safe" refuses lanes whose
+    values would overflow or leave the normal range."""
+    import torch
+    if mode not in _lib.BACKSCALE:
+        raise ValueError("unknown backscale mode %r" % (mode,))
+    host = not is_device_array(smax_scaled)
+    device = (smax_scaled.device if not host
+              else torch.device("cuda", torch.cuda.current_device()))
+    ins = [_to_device(np.atleast_1d(x) if host else x, device)
+           for x in (smax_scaled, smin_scaled, shift)]
+    n = int(ins[0].numel())
+    outs = [torch.empty(n, dtype=torch.float64, device=device)
+            for _ in range(3)]
+    rc = _lib.lib.b2s_backscale(n, *[_addr(x) for x in ins],
+                                _lib.BACKSCALE[mode],
+                                *[_addr(x) for x in outs], _stream_of(ins[0]))
+    _lib.check(rc, "b2s_backscale")
+    if host:
+        return tuple(o.cpu().numpy() for o in outs)
+    return tuple(outs)

@@ -1,0 +1,220 @@
+"""GPU parity: the sm_100a kernels vs the reference, bit for bit.
+
+Every comparison goes through the C-ABI (libb2s.so) via the package's
+public API.  Ground truth is the reference's own output (tests/golden/,
+made by running lanesvd) and, for arbitrary inputs, the oracle pinned to it.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import assert_bits_equal, digest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2005_07403_b200 as b2s  # noqa: E402
+from paper_2005_07403_b200 import _lib, synth  # noqa: E402
+from paper_2005_07403_b200.layout import Batch2x2, from_trains  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+RECORD_MODES = {"patterned_real_safe": ("safe", False),
+                "fuzz_real_safe": ("safe", False),
+                "fuzz_real_unc": ("unconditional", False),
+                "fuzz_real_sine": ("none", True),
+                "fuzz_complex_sine": ("none", True)}
+
+
+def _dev_batch(re, im):
+    b = from_trains(re, im)
+    return b.to(DEV)
+
+
+def _host_digests(out):
+    return {k: digest(v.cpu().numpy() if hasattr(v, "cpu") else v)
+            for k, v in out.trains().items()}
+
+
+def test_device_fp_env():
+    assert _lib.lib.b2s_check_fp_env(0) == 0
+
+
+def test_lane_records_device_path(lanes):
+    for name, rec in lanes.items():
+        mode, sine = RECORD_MODES.get(name, ("none", False))
+        re, im = rec["in_re"], rec.get("in_im")
+        b = _dev_batch(re, im)
+        out, wall = b2s.run_batch(b, b2s.RunConfig(field=b.field, backscale_mode=mode),
+                                  sine_form=sine)
+        assert wall > 0
+        host = out.cpu()
+        n = re.shape[1]
+        for k, arr in host.trains().items():
+            got = arr[..., :n]
+            assert_bits_equal(got, rec[k][..., :n], "%s/%s" % (name, k))
+
+
+def test_lane_records_host_path(lanes):
+    for name, rec in lanes.items():
+        mode, sine = RECORD_MODES.get(name, ("none", False))
+        b = from_trains(rec["in_re"], rec.get("in_im"))
+        out, _ = b2s.run_batch(b, b2s.RunConfig(field=b.field, backscale_mode=mode),
+                               sine_form=sine)
+        n = rec["in_re"].shape[1]
+        for k, arr in out.trains().items():
+            assert_bits_equal(arr[..., :n], rec[k][..., :n], "%s/%s" % (name, k))
+
+
+def test_state_dump_matches_reference(lanes):
+    for name, rec in lanes.items():
+        if "states" not in rec:
+            continue
+        parts = [rec["in_re"][t] for t in range(4)]
+        if "in_im" in rec:
+            parts = [x for t in range(4) for x in (rec["in_re"][t], rec["in_im"][t])]
+        _, states = b2s.svd2_lanes(tuple(parts), with_states=True)
+        got = np.stack(states.trains())
+        assert_bits_equal(got, rec["states"], name + "/states")
+
+
+@pytest.mark.parametrize("config", [0, 1, 2])
+def test_full_config_digests(digests, config):
+    entry = digests["configs"][str(config)]
+    n = entry["n"]
+    re, im = synth.generate_device(config, digests["seed"], 0, n, device=DEV)
+    assert digest(re.cpu().numpy()) == entry["input"]["re"], "device synth drifted"
+    if im is not None:
+        assert digest(im.cpu().numpy()) == entry["input"]["im"]
+    b = Batch2x2(n=n, re=re, im=im)
+    for key in ("none", "safe", "unconditional", "sine"):
+        if key not in entry:
+            continue
+        mode = key if key in ("safe", "unconditional") else "none"
+        out, _ = b2s.run_batch(b, b2s.RunConfig(field=b.field, backscale_mode=mode),
+                               sine_form=key == "sine")
+        assert _host_digests(out) == entry[key], (config, key)
+
+
+@pytest.mark.parametrize("config", [3, 4])
+def test_large_config_windows(digests, config):
+    entry = digests["configs"][str(config)]
+    W = digests["window"]
+    for w in entry["windows"]:
+        re, im = synth.generate_device(config, digests["seed"], w["lo"], W, device=DEV)
+        assert digest(re.cpu().numpy()) == w["input"]["re"]
+        out, _ = b2s.run_batch(Batch2x2(n=W, re=re, im=im),
+                               b2s.RunConfig(field="real" if im is None else "complex"))
+        assert _host_digests(out) == w["none"], (config, w["lo"])
+
+
+@pytest.mark.parametrize("config", [0, 1, 2, 3, 4])
+def test_device_synth_equals_host_synth(config):
+    for lo, n in ((0, 4096), (123456, 1000), (5, 77)):
+        hr, hi = synth.generate(config, 99, lo, n)
+        dr, di = synth.generate_device(config, 99, lo, n, device=DEV)
+        assert_bits_equal(dr.cpu().numpy(), hr, "re")
+        if hi is not None:
+            assert_bits_equal(di.cpu().numpy(), hi, "im")
+
+
+@pytest.mark.parametrize("field", ["real", "complex"])
+def test_fuzz_vs_oracle_1m(field):
+    rng = np.random.default_rng(11)
+    k = 8 if field == "complex" else 4
+    n = 1 << 20
+    v = rng.integers(0, 2 ** 64, size=(k, n), dtype=np.uint64).view(np.float64).copy()
+    v[~np.isfinite(v)] = 1.0
+    v[rng.random((k, n)) < 0.1] = 0.0
+    re, im = (v[0::2], v[1::2]) if field == "complex" else (v, None)
+    ref = oracle.svd2(re, im)
+    out, _ = b2s.run_batch(_dev_batch(re, im), b2s.RunConfig(field=field))
+    host = out.cpu()
+    for name, arr in ref.trains().items():
+        assert_bits_equal(host.trains()[name], arr, name)
+
+
+def test_backscale_kernel_vs_oracle():
+    rng = np.random.default_rng(5)
+    n = 1 << 16
+    smax = np.abs(rng.standard_normal(n)) * np.exp2(rng.integers(-1074, 1023, n))
+    smin = smax * rng.random(n)
+    smin[::7] = 0.0
+    shift = rng.integers(-2, 2096, n).astype(np.float64)
+    shift[::11] = 1.7976931348623157e308
+    for mode in ("none", "safe", "unconditional"):
+        ref = oracle.backscale(smax, smin, shift, mode)
+        got = b2s.backscale(smax, smin, shift, mode)
+        for r, g in zip(ref, got):
+            assert_bits_equal(g, r, mode)
+
+
+def test_partition_and_shard_invariance():
+    re, _ = synth.generate_device(3, 1, 0, 1 << 20, device=DEV)
+    b = Batch2x2(n=1 << 20, re=re)
+    whole, _ = b2s.run_batch(b, b2s.RunConfig())
+    lo = Batch2x2(n=1 << 19, re=re[:, : 1 << 19].contiguous())
+    hi = Batch2x2(n=1 << 19, re=re[:, 1 << 19:].contiguous())
+    a, _ = b2s.run_batch(lo, b2s.RunConfig())
+    c, _ = b2s.run_batch(hi, b2s.RunConfig())
+    assert torch.equal(torch.cat([a.u_re, c.u_re], 1).view(torch.int64), whole.u_re.view(torch.int64))
+    assert torch.equal(torch.cat([a.smax, c.smax]).view(torch.int64), whole.smax.view(torch.int64))
+
+
+def test_repeat_determinism():
+    re, im = synth.generate_device(4, 2, 0, 1 << 18, device=DEV)
+    b = Batch2x2(n=1 << 18, re=re, im=im)
+    a, _ = b2s.run_batch(b, b2s.RunConfig(field="complex"))
+    c, _ = b2s.run_batch(b, b2s.RunConfig(field="complex"))
+    for k in a.trains():
+        assert torch.equal(a.trains()[k].view(torch.int64), c.trains()[k].view(torch.int64))
+
+
+def test_host_pipeline_chunks_equal_device():
+    n = 300_000
+    re, im = synth.generate(1, 4, 0, n)
+    b = from_trains(re, im)
+    ref = oracle.svd2(b.re, b.im)
+    for chunk in (0, 4096, 65536 + 8):
+        out, _ = b2s.run_batch(b, b2s.RunConfig(field="complex", chunk=chunk))
+        for k, arr in ref.trains().items():
+            assert_bits_equal(out.trains()[k], arr, "%s chunk=%d" % (k, chunk))
+
+
+def test_chunk_and_single_entry_points():
+    re = np.zeros((4, 8))
+    re[0] = 1.0
+    re[3] = 1.0
+    res = b2s.svd2_chunk(re)
+    assert (res.shift == 1021.0).all() and (res.smax == 2.0 ** 1021).all()
+    a = np.array([[1 + 1j, 0], [0, 2 - 1j]])
+    one = b2s.svd2_single(a)
+    assert one.u.dtype == np.complex128
+    s = np.array([one.smax, one.smin]) * 2.0 ** -one.shift
+    rec = one.u @ np.diag(s) @ one.v.conj().T
+    assert np.abs(rec - a).max() < 1e-15 * np.abs(a).max()
+
+
+def test_padding_lanes_and_empty_batch():
+    b = b2s.pack(np.random.default_rng(1).standard_normal((5, 2, 2)))
+    out, _ = b2s.run_batch(b, b2s.RunConfig())
+    assert (out.smax[5:] == 0.0).all()
+    assert (out.shift[5:] == 1.7976931348623157e308).all()
+    empty = b2s.pack(np.zeros((0, 2, 2)))
+    out, wall = b2s.run_batch(empty, b2s.RunConfig())
+    assert out.n == 0 and out.n_hat == 0
+
+
+def test_invalid_arguments_raise_valueerror():
+    b = b2s.pack(np.eye(2).reshape(1, 2, 2))
+    with pytest.raises(ValueError):
+        b2s.run_batch(b, b2s.RunConfig(field="complex"))
+    with pytest.raises(TypeError):
+        b2s.run_batch(b.re, b2s.RunConfig())
+    with pytest.raises(ValueError):
+        b2s.svd2_lanes((np.zeros(3), np.zeros(3)))
+    with pytest.raises(ValueError):
+        b2s.backscale(np.ones(1), np.ones(1), np.zeros(1), mode="maybe")

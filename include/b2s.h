@@ -18,8 +18,11 @@
  * b2s_last_error() gives a thread-local message for the last failure.
  *
  * Device entry points are asynchronous on the given stream (cudaStream_t
- * passed as void*; NULL = legacy default stream) and perform no allocation.
- * All are reentrant; call them from one host thread per GPU.
+ * passed as void*; NULL = legacy default stream).  Their only allocation is
+ * a per-device hard-lane bit mask (4 bytes per 32 lanes, <= 256 MiB), made
+ * on first use and reused;
+ * b2s_reserve_workspace() makes it ahead of time (e.g. before CUDA-graph
+ * capture).  All are reentrant; call them from one host thread per GPU.
  */
 #ifndef B2S_H
 #define B2S_H
@@ -113,11 +116,43 @@ int b2s_synth(int config, uint64_t seed, int64_t lane0, int64_t n,
               double *const re[4], double *const im[4], void *stream);
 
 /*
+ * Pre-allocate the per-device hard-lane mask for launches of up to `lanes`
+ * lanes.  The fast kernels evaluate every division / sqrt with inline
+ * sequences whose operand ranges the scaling phase guarantees; lanes whose
+ * operands leave them (tiny ratios, subnormal entries, zero matrices) are
+ * marked and recomputed with IEEE intrinsics by a fix-up kernel.
+ */
+int b2s_reserve_workspace(int device, int64_t lanes);
+
+/*
+ * Number of hard lanes (recomputed exactly) in the most recent real or
+ * complex device launch on `device`; synchronises the device.  -1 on error.
+ */
+long long b2s_hard_lane_count(int device);
+
+/*
  * Device floating-point environment canary, the GPU analogue of
  * lanes.assert_fp_env (lanes.py:274-302): round-to-nearest-even, gradual
  * underflow and a fused fma on `device`.  Blocking.  0 = environment OK.
  */
 int b2s_check_fp_env(int device);
+
+/*
+ * Diagnostic probe of the engine's inline arithmetic, element-wise on
+ * device arrays (used by the GPU tests to prove the fast sequences
+ * bit-identical to IEEE operations):
+ *   0 a / b via the fast reciprocal + residual sequence (no range check)
+ *   1 sqrt(a)   2 1/a   3 1/sqrt(a) (two roundings, lanes.py:230-232)
+ *   4 hypot_lane(a, b) (lanes.py:213-227), magnitudes < 2^1023
+ *   5 a * 2^b for integer b in [-2, 2095] (the scaling phase)
+ *   6 a / b for 0 <= a <= b < 2^1023 (checked site division)
+ *   7 / 8 cos / sin of phase_from_parts(a, b, hypot(a, b)) (lanes.py:248-259)
+ * Checked ops write the NaN pattern 0x7FF4DEADBEEF0000 where the fast path
+ * declines (the kernels recompute such lanes exactly).  b may be NULL for
+ * ops 1-3.
+ */
+int b2s_math_probe(int op, int64_t n, const double *a, const double *b,
+                   double *out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,8 @@ def lib():
             getattr(L, name).argtypes = [ctypes.c_double, ctypes.c_double]
             getattr(L, name).restype = ctypes.c_double
         L.oracle_backscale.argtypes = [i64, _P, _P, _P, c_int, _P, _P, _P]
+        L.oracle_hypot_vec.argtypes = [i64, _P, _P, _P]
+        L.oracle_phase_vec.argtypes = [i64, _P, _P, _P, _P]
         _lib = L
     return _lib
 
@@ -158,3 +160,19 @@ def hypot(a, b):
 
 def invsqrt(a):
     return lib().oracle_invsqrt(float(a))
+
+
+def hypot_vec(a, b):
+    """lanes.hypot_lane elementwise (lanes.py:213-227)."""
+    a, b = (np.ascontiguousarray(x, dtype=np.float64) for x in (a, b))
+    out = np.empty_like(a)
+    lib().oracle_hypot_vec(a.size, _ptr(a), _ptr(b), _ptr(out))
+    return out
+
+
+def phase_vec(re, im):
+    """lanes.polar's (cos, sin) elementwise (lanes.py:248-270)."""
+    re, im = (np.ascontiguousarray(x, dtype=np.float64) for x in (re, im))
+    c, s = np.empty_like(re), np.empty_like(re)
+    lib().oracle_phase_vec(re.size, _ptr(re), _ptr(im), _ptr(c), _ptr(s))
+    return c, s

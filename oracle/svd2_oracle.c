@@ -497,3 +497,19 @@ void oracle_backscale(int64_t n, const double *smax, const double *smin,
         backscale(smax[k], smin[k], shift[k], mode, &omax[k], &omin[k],
                   &oshift[k]);
 }
+
+/* vectorised probes for the GPU arithmetic tests */
+void oracle_hypot_vec(int64_t n, const double *a, const double *b, double *out)
+{
+    for (int64_t k = 0; k < n; k++) out[k] = hypot_lane(a[k], b[k]);
+}
+
+/* lanes.py:262-270 polar(): magnitude and unit phase */
+void oracle_phase_vec(int64_t n, const double *re, const double *im,
+                      double *c, double *s)
+{
+    for (int64_t k = 0; k < n; k++) {
+        double mag = hypot_lane(re[k], im[k]);
+        phase_from_parts(re[k], im[k], mag, &c[k], &s[k]);
+    }
+}

@@ -3,7 +3,7 @@
 The CUDA library is the only compute path: if it is missing this module
 raises at import, there is no CPU fallback.  Build it with
 ``python -c "import __graft_entry__ as g; g.build()"`` (or
-``python -m paper_2005_07403_b200.build``).
+``python paper_2005_07403_b200/build.py``).
 """
 
 from __future__ import annotations
@@ -25,7 +25,8 @@ STATES_COMPLEX = 20
 SYMBOLS = (
     "b2s_version", "b2s_last_error", "b2s_svd2_real", "b2s_svd2_complex",
     "b2s_svd2_real_host", "b2s_svd2_complex_host", "b2s_backscale",
-    "b2s_synth", "b2s_check_fp_env",
+    "b2s_synth", "b2s_check_fp_env", "b2s_math_probe",
+    "b2s_reserve_workspace", "b2s_hard_lane_count",
 )
 
 _P = ctypes.c_void_p
@@ -56,9 +57,13 @@ def _load():
     L.b2s_backscale.argtypes = [_i64, _P, _P, _P, _int, _P, _P, _P, _P]
     L.b2s_synth.argtypes = [_int, ctypes.c_uint64, _i64, _i64, _PA, _PA, _P]
     L.b2s_check_fp_env.argtypes = [_int]
+    L.b2s_math_probe.argtypes = [_int, _i64, _P, _P, _P, _P]
+    L.b2s_reserve_workspace.argtypes = [_int, _i64]
+    L.b2s_hard_lane_count.argtypes = [_int]
     for name in SYMBOLS:
         if name not in ("b2s_version", "b2s_last_error"):
             getattr(L, name).restype = _int
+    L.b2s_hard_lane_count.restype = ctypes.c_longlong
     return L
 
 

@@ -1,4 +1,4 @@
-"""Build the native engine in-tree: ``python -m paper_2005_07403_b200.build``.
+"""Build the native engine in-tree: ``python paper_2005_07403_b200/build.py``.
 
 One nvcc invocation compiles the CUDA sources for sm_100a only
 (``-gencode arch=compute_100a,code=sm_100a``) into ``_native/libb2s.so``.
@@ -14,7 +14,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = ["csrc/b2s_kernels.cu", "csrc/b2s_synth.cu", "csrc/b2s_host.cu"]
-HEADERS = ["csrc/b2s_lane.cuh", "csrc/b2s_svd2.cuh", "csrc/b2s_common.cuh",
+HEADERS = ["csrc/b2s_lane.cuh", "csrc/b2s_svd2.cuh", "csrc/b2s_fast.cuh", "csrc/b2s_common.cuh",
            "../include/b2s.h"]
 OUT = os.path.join(HERE, "_native", "libb2s.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",

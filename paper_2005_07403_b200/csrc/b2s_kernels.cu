@@ -8,7 +8,9 @@
 // every thread keeps one lane of loads in flight behind its arithmetic.
 #include "../../include/b2s.h"
 #include "b2s_common.cuh"
-#include "b2s_svd2.cuh"
+#include "b2s_fast.cuh"
+
+#include <mutex>
 
 namespace b2s {
 
@@ -17,7 +19,18 @@ char* last_error_buf() {
   return buf;
 }
 
+// Per-launch hard-lane mask: bit l of word w marks lane 32w + l as hard
+// (its operands left a fast call site's proven range).  The fast kernel
+// writes one ballot word per warp-iteration -- no atomics, 4 bytes per 32
+// lanes of traffic -- and the fix-up kernel compacts the set bits and
+// recomputes those lanes, packed, with exact arithmetic.
+struct HardQueue {
+  unsigned* mask;
+  unsigned long long* cnt;   // hard lanes found by the fix-up (diagnostics)
+};
+
 struct RealArgs {
+  HardQueue q;
   int64_t n;
   const double* a[4];
   double* u[4];
@@ -27,6 +40,7 @@ struct RealArgs {
 };
 
 struct CplxArgs {
+  HardQueue q;
   int64_t n;
   const double* ar[4];
   const double* ai[4];
@@ -61,8 +75,60 @@ __device__ __forceinline__ void store_states(double* const* st, int64_t i, const
   st_stream(st[k++] + i, s.smin);
 }
 
+template <int Mode>
+__device__ __forceinline__ void store_real(const RealArgs& A, int64_t i, RealOut o) {
+  backscale_lane<Mode>(o.smax, o.smin, o.shift);
+  #pragma unroll
+  for (int t = 0; t < 4; t++) st_stream(A.u[t] + i, o.u[t]);
+  #pragma unroll
+  for (int t = 0; t < 4; t++) st_stream(A.v[t] + i, o.v[t]);
+  st_stream(A.smax + i, o.smax);
+  st_stream(A.smin + i, o.smin);
+  st_stream(A.shift + i, o.shift);
+}
+
+template <int Mode>
+__device__ __forceinline__ void store_cplx(const CplxArgs& A, int64_t i, CplxOut o) {
+  backscale_lane<Mode>(o.smax, o.smin, o.shift);
+  #pragma unroll
+  for (int t = 0; t < 4; t++) { st_stream(A.ur[t] + i, o.ur[t]); st_stream(A.ui[t] + i, o.ui[t]); }
+  #pragma unroll
+  for (int t = 0; t < 4; t++) { st_stream(A.vr[t] + i, o.vr[t]); st_stream(A.vi[t] + i, o.vi[t]); }
+  st_stream(A.smax + i, o.smax);
+  st_stream(A.smin + i, o.smin);
+  st_stream(A.shift + i, o.shift);
+}
+
+// A marked lane again, with every failing call site re-evaluated exactly.
+template <int Mode, bool Sine>
+__device__ __forceinline__ void redo_real(const RealArgs& A, int64_t i) {
+  double a[4];
+  #pragma unroll
+  for (int t = 0; t < 4; t++) a[t] = A.a[t][i];
+  RealOut o;
+  svd2_real_f<Sine, true>(a, o);
+  store_real<Mode>(A, i, o);
+}
+
+template <int Mode, bool Sine>
+__device__ __forceinline__ void redo_cplx(const CplxArgs& A, int64_t i) {
+  double ar[4], ai[4];
+  #pragma unroll
+  for (int t = 0; t < 4; t++) { ar[t] = A.ar[t][i]; ai[t] = A.ai[t][i]; }
+  CplxOut o;
+  svd2_complex_f<Sine, true>(ar, ai, o);
+  store_cplx<Mode>(A, i, o);
+}
+
+// Record this warp's hard lanes: one ballot word per 32 consecutive lanes.
+// Lane 0 of the warp always holds the lowest (32-aligned) index.
+__device__ __forceinline__ void mark_hard(const HardQueue& q, bool hard, int64_t i) {
+  const unsigned m = __ballot_sync(__activemask(), hard);
+  if ((threadIdx.x & 31) == 0) q.mask[i >> 5] = m;
+}
+
 template <int Mode, bool Sine, bool States>
-__global__ void __launch_bounds__(kBlock) k_svd2_real(const RealArgs A) {
+__global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= A.n) return;
@@ -77,22 +143,21 @@ __global__ void __launch_bounds__(kBlock) k_svd2_real(const RealArgs A) {
       for (int t = 0; t < 4; t++) nx[t] = ld_stream(A.a[t] + j);
     }
     RealOut o;
-    LaneStates s;
-    svd2_real<Sine, States>(a, o, &s);
-    backscale_lane<Mode>(o.smax, o.smin, o.shift);
-    #pragma unroll
-    for (int t = 0; t < 4; t++) st_stream(A.u[t] + i, o.u[t]);
-    #pragma unroll
-    for (int t = 0; t < 4; t++) st_stream(A.v[t] + i, o.v[t]);
-    st_stream(A.smax + i, o.smax);
-    st_stream(A.smin + i, o.smin);
-    st_stream(A.shift + i, o.shift);
-    if (States) store_states<false>(A.st, i, s);
+    if (States) {
+      LaneStates s;
+      svd2_real_x<Sine, true>(a, o, &s);
+      store_real<Mode>(A, i, o);
+      store_states<false>(A.st, i, s);
+    } else {
+      const bool hard = svd2_real_f<Sine, false>(a, o);
+      store_real<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
+      mark_hard(A.q, hard, i);
+    }
   }
 }
 
 template <int Mode, bool Sine, bool States>
-__global__ void __launch_bounds__(kBlock) k_svd2_complex(const CplxArgs A) {
+__global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= A.n) return;
@@ -108,18 +173,65 @@ __global__ void __launch_bounds__(kBlock) k_svd2_complex(const CplxArgs A) {
       for (int t = 0; t < 4; t++) { nr[t] = ld_stream(A.ar[t] + j); ni[t] = ld_stream(A.ai[t] + j); }
     }
     CplxOut o;
-    LaneStates s;
-    svd2_complex<Sine, States>(ar, ai, o, &s);
-    backscale_lane<Mode>(o.smax, o.smin, o.shift);
-    #pragma unroll
-    for (int t = 0; t < 4; t++) { st_stream(A.ur[t] + i, o.ur[t]); st_stream(A.ui[t] + i, o.ui[t]); }
-    #pragma unroll
-    for (int t = 0; t < 4; t++) { st_stream(A.vr[t] + i, o.vr[t]); st_stream(A.vi[t] + i, o.vi[t]); }
-    st_stream(A.smax + i, o.smax);
-    st_stream(A.smin + i, o.smin);
-    st_stream(A.shift + i, o.shift);
-    if (States) store_states<true>(A.st, i, s);
+    if (States) {
+      LaneStates s;
+      svd2_complex_x<Sine, true>(ar, ai, o, &s);
+      store_cplx<Mode>(A, i, o);
+      store_states<true>(A.st, i, s);
+    } else {
+      const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
+      store_cplx<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
+      mark_hard(A.q, hard, i);
+    }
   }
+}
+
+// Exact fix-up of the marked hard lanes.  Each warp takes 32 mask words
+// (1024 lanes) at a time, compacts their set bits into a shared-memory list
+// with a warp prefix sum, then recomputes the listed lanes 32 at a time.
+constexpr int kFixWarps = kBlock / 32;
+
+template <typename Redo>
+__device__ __forceinline__ void fix_lanes(const HardQueue& q, int64_t n, Redo redo) {
+  __shared__ unsigned list[kFixWarps][1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t words = (n + 31) >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * kFixWarps;
+  unsigned long long found = 0;
+  for (int64_t base = ((int64_t)blockIdx.x * kFixWarps + warp) * 32; base < words; base += nwarps * 32) {
+    const unsigned w = (base + lane < words) ? q.mask[base + lane] : 0u;
+    const int c = __popc(w);
+    int incl = c;
+    #pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (total == 0) continue;
+    int pos = incl - c;
+    unsigned bitsleft = w;
+    while (bitsleft) {
+      const int b = __ffs(bitsleft) - 1;
+      bitsleft &= bitsleft - 1;
+      list[warp][pos++] = (unsigned)(((base + lane) << 5) + b);
+    }
+    __syncwarp();
+    for (int j = lane; j < total; j += 32) redo((int64_t)list[warp][j]);
+    __syncwarp();
+    found += (unsigned long long)total;
+  }
+  if (lane == 0 && found) atomicAdd(q.cnt, found);
+}
+
+template <int Mode, bool Sine>
+__global__ void __launch_bounds__(kBlock) k_fix_real(const RealArgs A) {
+  fix_lanes(A.q, A.n, [&](int64_t i) { redo_real<Mode, Sine>(A, i); });
+}
+
+template <int Mode, bool Sine>
+__global__ void __launch_bounds__(kBlock) k_fix_cplx(const CplxArgs A) {
+  fix_lanes(A.q, A.n, [&](int64_t i) { redo_cplx<Mode, Sine>(A, i); });
 }
 
 template <int Mode>
@@ -133,6 +245,30 @@ __global__ void __launch_bounds__(kBlock) k_backscale(int64_t n, const double* s
     omax[i] = a;
     omin[i] = b;
     oshift[i] = s;
+  }
+}
+
+// Element-wise probe of the engine's inline arithmetic (tests only).  Ops
+// with a range-check flag write kHardMarker where the fast path declines.
+__device__ __forceinline__ double hard_marker() { return dbl(0x7FF4DEADBEEF0000ull); }
+
+__global__ void __launch_bounds__(kBlock) k_math_probe(int op, int64_t n, const double* a, const double* b,
+                                                      double* o) {
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride) {
+    double x = a[i], y = b ? b[i] : 0.0, r;
+    bool hard = false;
+    switch (op) {
+      case 0: r = quot_f(x, y, rcp_f(y)); break;
+      case 1: r = sqrt_f(x); break;
+      case 2: r = rcp_f(x); break;
+      case 3: r = invsqrt_f(x); break;
+      case 4: r = hypot_big_f<false>(fabs_(x), fabs_(y), hard); break;
+      case 5: r = scale_up(x, (int)y); break;
+      case 6: r = div_pos_big_f<false>(x, y, hard); break;
+      default: { double c, s; phase_f<false>(x, y, hypot_x(x, y), c, s, hard); r = (op == 7) ? c : s; } break;
+    }
+    o[i] = hard ? hard_marker() : r;
   }
 }
 
@@ -163,21 +299,96 @@ static int resident_grid(K kernel, int64_t n) {
   return grid_for(kernel, kBlock, n, &err);
 }
 
-template <int Mode, bool Sine, bool States>
-static int launch_real(const RealArgs& A, cudaStream_t s) {
-  auto k = k_svd2_real<Mode, Sine, States>;
-  int grid = resident_grid(k, A.n);
-  k<<<grid, kBlock, 0, s>>>(A);
-  B2S_CUDA(cudaGetLastError());
+// Per-device hard-lane mask storage (4 bytes per 32 lanes of one
+// sub-launch), allocated on first use and grown on demand;
+// b2s_reserve_workspace pre-allocates (e.g. before CUDA-graph capture).
+struct Workspace {
+  std::mutex mu;
+  unsigned* mask = nullptr;
+  unsigned long long* cnt = nullptr;
+  size_t words = 0;
+};
+
+static Workspace& workspace(int dev) {
+  static Workspace ws[64];
+  return ws[dev & 63];
+}
+
+constexpr int64_t kMaxLaunch = int64_t(1) << 31;     // lanes per sub-launch
+
+static int get_queue(int64_t n, HardQueue* q) {
+  int dev = 0;
+  B2S_CUDA(cudaGetDevice(&dev));
+  Workspace& w = workspace(dev);
+  std::lock_guard<std::mutex> lock(w.mu);
+  size_t want = (size_t)((n + 31) / 32);
+  if (want < 4096) want = 4096;
+  if (!w.cnt) B2S_CUDA(cudaMalloc(&w.cnt, sizeof(unsigned long long)));
+  if (w.words < want) {
+    if (w.mask) cudaFree(w.mask);
+    w.mask = nullptr;
+    w.words = 0;
+    B2S_CUDA(cudaMalloc(&w.mask, want * sizeof(unsigned)));
+    w.words = want;
+  }
+  q->mask = w.mask;
+  q->cnt = w.cnt;
   return 0;
 }
 
 template <int Mode, bool Sine, bool States>
-static int launch_cplx(const CplxArgs& A, cudaStream_t s) {
-  auto k = k_svd2_complex<Mode, Sine, States>;
-  int grid = resident_grid(k, A.n);
-  k<<<grid, kBlock, 0, s>>>(A);
-  B2S_CUDA(cudaGetLastError());
+static int launch_real(RealArgs A, cudaStream_t s) {
+  const int64_t total = A.n;
+  const RealArgs base = A;
+  for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
+    A = base;
+    A.n = (total - lo) < kMaxLaunch ? (total - lo) : kMaxLaunch;
+    for (int t = 0; t < 4; t++) { A.a[t] += lo; A.u[t] += lo; A.v[t] += lo; }
+    A.smax += lo; A.smin += lo; A.shift += lo;
+    if (States) for (int k = 0; k < B2S_STATES_REAL; k++) A.st[k] += lo;
+    if (!States) {
+      int rc = get_queue(A.n, &A.q);
+      if (rc) return rc;
+      B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
+    }
+    auto k = k_svd2_real<Mode, Sine, States>;
+    k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
+    B2S_CUDA(cudaGetLastError());
+    if (!States) {
+      auto f = k_fix_real<Mode, Sine>;
+      f<<<resident_grid(f, (int64_t)kBlock * 148 * 4), kBlock, 0, s>>>(A);
+      B2S_CUDA(cudaGetLastError());
+    }
+  }
+  return 0;
+}
+
+template <int Mode, bool Sine, bool States>
+static int launch_cplx(CplxArgs A, cudaStream_t s) {
+  const int64_t total = A.n;
+  const CplxArgs base = A;
+  for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
+    A = base;
+    A.n = (total - lo) < kMaxLaunch ? (total - lo) : kMaxLaunch;
+    for (int t = 0; t < 4; t++) {
+      A.ar[t] += lo; A.ai[t] += lo; A.ur[t] += lo; A.ui[t] += lo; A.vr[t] += lo; A.vi[t] += lo;
+    }
+    A.smax += lo; A.smin += lo; A.shift += lo;
+    if (States) for (int k = 0; k < B2S_STATES_COMPLEX; k++) A.st[k] += lo;
+    if (!States) {
+      int rc = get_queue(A.n, &A.q);
+      if (rc) return rc;
+      B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
+    }
+    auto k = k_svd2_complex<Mode, Sine, States>;
+    k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
+    B2S_CUDA(cudaGetLastError());
+    if (!States) {
+      auto f = k_fix_cplx<Mode, Sine>;
+      f<<<resident_grid(f, (int64_t)kBlock * 148 * 4), kBlock, 0, s>>>(A);
+      B2S_CUDA(cudaGetLastError());
+    }
+  }
   return 0;
 }
 
@@ -308,6 +519,48 @@ int b2s_backscale(int64_t n, const double* smax, const double* smin, const doubl
   }
   B2S_CUDA(cudaGetLastError());
   return 0;
+}
+
+int b2s_math_probe(int op, int64_t n, const double* a, const double* b, double* out, void* stream) {
+  if (op < 0 || op > 8) return fail(1, "unknown probe op %d", op);
+  if (n < 0) return fail(1, "negative n");
+  if (!a || !out || ((op == 0 || op >= 4) && !b)) return fail(5, "NULL operand");
+  if (n == 0) return 0;
+  int err = 0;
+  int g = grid_for(k_math_probe, kBlock, n, &err);
+  k_math_probe<<<g, kBlock, 0, (cudaStream_t)stream>>>(op, n, a, b, out);
+  B2S_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int b2s_reserve_workspace(int device, int64_t lanes) {
+  if (lanes < 0) return fail(1, "negative lane count");
+  if (lanes > kMaxLaunch) lanes = kMaxLaunch;
+  int prev = 0;
+  B2S_CUDA(cudaGetDevice(&prev));
+  B2S_CUDA(cudaSetDevice(device));
+  HardQueue q;
+  int rc = get_queue(lanes, &q);
+  cudaSetDevice(prev);
+  return rc;
+}
+
+long long b2s_hard_lane_count(int device) {
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return -1;
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  Workspace& w = workspace(device);
+  unsigned long long c = 0;
+  long long out = 0;
+  if (w.cnt) {
+    if (cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(&c, w.cnt, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess)
+      out = -1;
+    else
+      out = (long long)c;
+  }
+  cudaSetDevice(prev);
+  return out;
 }
 
 int b2s_check_fp_env(int device) {

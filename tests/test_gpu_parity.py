@@ -218,3 +218,16 @@ def test_invalid_arguments_raise_valueerror():
         b2s.svd2_lanes((np.zeros(3), np.zeros(3)))
     with pytest.raises(ValueError):
         b2s.backscale(np.ones(1), np.ones(1), np.zeros(1), mode="maybe")
+
+
+def test_hard_lane_queue_counts():
+    """Moderate-exponent configs take the fast path on (nearly) every lane;
+    config 2 (full exponent range, structured zeros) queues many lanes for
+    the exact fix-up -- results are bit-identical either way (digest tests)."""
+    for config, n, bound in ((3, 1 << 20, 1e-3), (1, 1 << 20, 1e-3), (2, 1 << 20, 1.0)):
+        re, im = synth.generate_device(config, 5, 0, n, device=DEV)
+        b2s.run_batch(Batch2x2(n=n, re=re, im=im),
+                      b2s.RunConfig(field="real" if im is None else "complex"))
+        c = _lib.lib.b2s_hard_lane_count(0)
+        assert 0 <= c <= bound * n, (config, c)
+        print("config %d: %d hard lanes of %d" % (config, c, n))

@@ -115,31 +115,24 @@ class Clocks:
 
 
 def dist_init():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2005_07403_b200.dist import world_info
+    world, rank, local = world_info()
     if world > 1:
-        import torch.distributed as dist
         import torch
+        import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
 def max_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2005_07403_b200.dist import max_over_ranks as m
+    return m(x)
 
 
 def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    from paper_2005_07403_b200.dist import barrier as b
+    b()
 
 
 def cpu_sample_rate(config, budget_s=12.0, sample=1 << 22, threads=None):
@@ -168,7 +161,8 @@ def run_device(config, world, rank, local, steps, warmup):
     cfg = synth.CONFIGS[config]
     field = cfg["field"]
     n_total = cfg["n"]
-    lo, hi = b2s.shards(n_total, world)[rank]
+    from paper_2005_07403_b200.dist import rank_span
+    lo, hi = rank_span(n_total, rank, world)
     n = hi - lo
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -222,7 +216,8 @@ def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
     from paper_2005_07403_b200 import synth
     cfg = synth.CONFIGS[config]
     n_total = cfg["n"]
-    lo, hi = b2s.shards(n_total, world)[rank]
+    from paper_2005_07403_b200.dist import rank_span
+    lo, hi = rank_span(n_total, rank, world)
     n = min(hi - lo, max_lanes)
     n -= n % 8
     cplx = cfg["field"] == "complex"

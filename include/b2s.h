@@ -145,8 +145,10 @@ int b2s_check_fp_env(int device);
  *   1 sqrt(a)   2 1/a   3 1/sqrt(a) (two roundings, lanes.py:230-232)
  *   4 hypot_lane(a, b) (lanes.py:213-227), magnitudes < 2^1023
  *   5 a * 2^b for integer b in [-2, 2095] (the scaling phase)
- *   6 a / b for 0 <= a <= b < 2^1023 (checked site division)
+ *   6 a / b, exponent-normalised division (exact for all normal / zero a
+ *     and normal b, subnormal quotients included)
  *   7 / 8 cos / sin of phase_from_parts(a, b, hypot(a, b)) (lanes.py:248-259)
+ *   9 a / b for 0 <= a <= b < 2^1023 (the streaming kernels' checked site)
  * Checked ops write the NaN pattern 0x7FF4DEADBEEF0000 where the fast path
  * declines (the kernels recompute such lanes exactly).  b may be NULL for
  * ops 1-3.

@@ -19,6 +19,15 @@
 
 namespace b2s {
 
+// Fix-mode repair of one failing division: the exponent-normalised division
+// (exact for every normal operand pair, subnormal quotients included), or
+// the IEEE intrinsic when an operand is subnormal.  Only called with a != 0.
+__device__ __forceinline__ double div_fix(double a, double b) {
+  bool h = false;
+  const double q = div_den<true>(a, make_den(b), h);
+  return h ? div_x(a, b) : q;
+}
+
 // (max, min) of two non-negative non-NaN magnitudes, one compare.  Equal
 // magnitudes have identical bits, so this matches relaxed_max / relaxed_min
 // (lanes.py:102-114) exactly on this domain.
@@ -37,7 +46,7 @@ __device__ __forceinline__ double div_pos_f(double a, double b, bool& hard) {
   const double d = z ? 1.0 : b;
   double q = quot_f(a, d, rcp_f(d));
   const bool h = !z && !(resid_ok(hi_(a)) && normal_q(hi_(q)));
-  if (Fix) { if (h) q = div_x(a, b); } else hard |= h;
+  if (Fix) { if (h) q = div_fix(a, b); } else hard |= h;
   return q;
 }
 
@@ -51,7 +60,7 @@ __device__ __forceinline__ double div_pos_big_f(double a, double b, bool& hard) 
   const double d = z ? 1.0 : mul(b, sc);
   double q = quot_f(a2, d, rcp_f(d));
   const bool h = !z && !(resid_ok(hi_(a2)) && normal_q(hi_(q)));
-  if (Fix) { if (h) q = div_x(a, b); } else hard |= h;
+  if (Fix) { if (h) q = div_fix(a, b); } else hard |= h;
   return q;
 }
 
@@ -70,7 +79,7 @@ __device__ __forceinline__ double hypot_f(double m1, double m2, bool& hard) {
   bool h = false;
   double q = div_pos_f<false>(small, big, h);   // = small / max(big, TRUE_MIN)
   h = h && !hypot_q_irrelevant(q);
-  if (Fix) { if (h) q = div_x(small, rmax(big, kTrueMin())); } else hard |= h;
+  if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
   return mul(big, sqrt_f(fma_(q, q, 1.0)));
 }
 
@@ -83,7 +92,7 @@ __device__ __forceinline__ double hypot_big_f(double m1, double m2, bool& hard) 
   bool h = false;
   double q = div_pos_big_f<false>(small, big, h);
   h = h && !hypot_q_irrelevant(q);
-  if (Fix) { if (h) q = div_x(small, rmax(big, kTrueMin())); } else hard |= h;
+  if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
   return mul(big, sqrt_f(fma_(q, q, 1.0)));
 }
 
@@ -108,8 +117,8 @@ __device__ __forceinline__ void phase_f(double re, double im, double mag, double
   const bool hc = nz_(a1) && !(resid_ok(hi_(a1)) && normal_q(hi_(q1)));
   const bool hs = nz_(im) && !(resid_ok(lop_and(hi_(a2), 0x7FFFFFFFu)) && normal_q(lop_and(hi_(q2), 0x7FFFFFFFu)));
   if (Fix) {
-    if (hc) c = or_(rmin(div_x(fabs_(re), mag), 1.0), sgn_(re));
-    if (hs) s = div_x(im, rmax(mag, kTrueMin()));
+    if (hc) c = or_(rmin(div_fix(fabs_(re), mag), 1.0), sgn_(re));
+    if (hs) s = div_fix(im, rmax(mag, kTrueMin()));
   } else {
     hard |= hc | hs;
   }
@@ -129,8 +138,8 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   const bool hx = nz_(r12) && !(resid_ok(hi_(a12)) && normal_q(hi_(qx)));
   const bool hy = nz_(r22) && !(resid_ok(hi_(a22)) && normal_q(hi_(qy)));
   if (Fix) {
-    if (hx) qx = div_x(r12, r11);
-    if (hy) qy = div_x(r22, r11);
+    if (hx) qx = div_fix(r12, r11);
+    if (hy) qy = div_fix(r22, r11);
   } else {
     hard |= hx | hy;
   }
@@ -142,7 +151,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   // num / den: num == 0 gives +0 or NaN (den == 0), both absorbed to +0.
   double qn = quot_f(num, den, rcp_f(den));
   const bool hn = nz_(num) && !(resid_ok(hi_(num)) && normal_q(hi_(qn)));
-  if (Fix) { if (hn) qn = div_x(num, den); } else hard |= hn;
+  if (Fix) { if (hn) qn = div_fix(num, den); } else hard |= hn;
   const double tan2 = or_(rmin(rmax(qn, 0.0), kSqrtDblMax()), kNegZero());
   // tan2 in [-sqrt(DBL_MAX), -0]; the denominator is in [2, 2^512].
   const double den2 = add(1.0, sqrt_f(fma_(tan2, tan2, 1.0)));
@@ -150,7 +159,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   double lt = mk_(lop_or(hi_(ql), 0x80000000u), lo_(ql));   // sign of -0 / den2
   const bool hl = nz_(tan2) && !(resid_ok(lop_and(hi_(tan2), 0x7FFFFFFFu)) &&
                                  normal_q(lop_and(hi_(ql), 0x7FFFFFFFu)));
-  if (Fix) { if (hl) lt = div_x(tan2, den2); } else hard |= hl;
+  if (Fix) { if (hl) lt = div_fix(tan2, den2); } else hard |= hl;
   const double ls2 = fma_(lt, lt, 1.0);
   const double rt = fma_(y, lt, -x);
   return triangle_tail(x, y, lt, r11, r22, invsqrt_f(ls2), invsqrt_f(fma_(rt, rt, 1.0)));

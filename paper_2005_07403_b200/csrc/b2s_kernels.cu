@@ -9,7 +9,9 @@
 #include "../../include/b2s.h"
 #include "b2s_common.cuh"
 #include "b2s_fast.cuh"
+#include "b2s_tma.cuh"
 
+#include <cstdlib>
 #include <mutex>
 
 namespace b2s {
@@ -186,6 +188,130 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged streaming kernels (the default when every train is 16-byte
+// aligned).  A persistent grid; each CTA walks its tiles of kBlock lanes
+// through a kStages-deep ring of shared-memory stages.  One thread arms the
+// stage's mbarrier and issues one cp.async.bulk per input train; the loads
+// of the next kStages-1 tiles are in flight while the CTA computes the
+// current one.  Outputs go straight from registers with streaming stores
+// (coalesced 256 B per warp per train).  The sub-tile tail is processed by
+// CTA 0 with ordinary loads.
+// ---------------------------------------------------------------------------
+constexpr int kStages = 4;
+
+template <int NT>
+struct TmaRing {
+  static constexpr uint32_t kTileBytes = kBlock * sizeof(double);
+  static constexpr size_t kSmem = (size_t)kStages * NT * kBlock * sizeof(double) + kStages * sizeof(uint64_t);
+  double* buf;      // [kStages][NT][kBlock]
+  uint64_t* bar;    // [kStages]
+  uint64_t pol;
+
+  __device__ __forceinline__ double* stage(int s, int t) { return buf + ((size_t)s * NT + t) * kBlock; }
+
+  __device__ __forceinline__ void init(char* smem) {
+    buf = reinterpret_cast<double*>(smem);
+    bar = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * NT * kBlock * sizeof(double));
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kStages; s++) tma::mbar_init(&bar[s], 1);
+      tma::fence_init();
+    }
+    __syncthreads();
+    pol = threadIdx.x == 0 ? tma::evict_first_policy() : 0;
+  }
+
+  // thread 0 only: fill stage s with tile `tile` of the NT trains src[]
+  __device__ __forceinline__ void issue(int s, const double* const* src, int64_t tile) {
+    tma::mbar_arrive_expect_tx(&bar[s], NT * kTileBytes);
+    #pragma unroll
+    for (int t = 0; t < NT; t++) tma::bulk_load(stage(s, t), src[t] + tile * kBlock, kTileBytes, &bar[s], pol);
+  }
+};
+
+template <int Mode, bool Sine>
+__global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
+  extern __shared__ __align__(128) char smem[];
+  TmaRing<4> R;
+  R.init(smem);
+  const int tid = threadIdx.x;
+  const int64_t tiles = A.n / kBlock;
+  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (tid == 0)
+    for (int s = 0; s < kStages && s < mine; s++) R.issue(s, A.a, blockIdx.x + (int64_t)s * gridDim.x);
+  for (int64_t k = 0; k < mine; k++) {
+    const int s = (int)(k % kStages);
+    tma::mbar_wait(&R.bar[s], (uint32_t)((k / kStages) & 1));
+    double a[4];
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = R.stage(s, t)[tid];
+    __syncthreads();                       // every thread has read stage s
+    if (tid == 0 && k + kStages < mine) {
+      tma::fence_proxy_async();
+      R.issue(s, A.a, blockIdx.x + (k + kStages) * gridDim.x);
+    }
+    const int64_t i = (blockIdx.x + k * gridDim.x) * kBlock + tid;
+    RealOut o;
+    const bool hard = svd2_real_f<Sine, false>(a, o);
+    store_real<Mode>(A, i, o);
+    mark_hard(A.q, hard, i);
+  }
+  if (blockIdx.x == 0) {
+    const int64_t i = tiles * kBlock + tid;
+    if (i < A.n) {
+      double a[4];
+      #pragma unroll
+      for (int t = 0; t < 4; t++) a[t] = A.a[t][i];
+      RealOut o;
+      const bool hard = svd2_real_f<Sine, false>(a, o);
+      store_real<Mode>(A, i, o);
+      mark_hard(A.q, hard, i);
+    }
+  }
+}
+
+template <int Mode, bool Sine>
+__global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
+  extern __shared__ __align__(128) char smem[];
+  TmaRing<8> R;
+  R.init(smem);
+  const double* src[8] = {A.ar[0], A.ar[1], A.ar[2], A.ar[3], A.ai[0], A.ai[1], A.ai[2], A.ai[3]};
+  const int tid = threadIdx.x;
+  const int64_t tiles = A.n / kBlock;
+  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (tid == 0)
+    for (int s = 0; s < kStages && s < mine; s++) R.issue(s, src, blockIdx.x + (int64_t)s * gridDim.x);
+  for (int64_t k = 0; k < mine; k++) {
+    const int s = (int)(k % kStages);
+    tma::mbar_wait(&R.bar[s], (uint32_t)((k / kStages) & 1));
+    double ar[4], ai[4];
+    #pragma unroll
+    for (int t = 0; t < 4; t++) { ar[t] = R.stage(s, t)[tid]; ai[t] = R.stage(s, 4 + t)[tid]; }
+    __syncthreads();
+    if (tid == 0 && k + kStages < mine) {
+      tma::fence_proxy_async();
+      R.issue(s, src, blockIdx.x + (k + kStages) * gridDim.x);
+    }
+    const int64_t i = (blockIdx.x + k * gridDim.x) * kBlock + tid;
+    CplxOut o;
+    const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
+    store_cplx<Mode>(A, i, o);
+    mark_hard(A.q, hard, i);
+  }
+  if (blockIdx.x == 0) {
+    const int64_t i = tiles * kBlock + tid;
+    if (i < A.n) {
+      double ar[4], ai[4];
+      #pragma unroll
+      for (int t = 0; t < 4; t++) { ar[t] = A.ar[t][i]; ai[t] = A.ai[t][i]; }
+      CplxOut o;
+      const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
+      store_cplx<Mode>(A, i, o);
+      mark_hard(A.q, hard, i);
+    }
+  }
+}
+
 // Exact fix-up of the marked hard lanes.  Each warp takes 32 mask words
 // (1024 lanes) at a time, compacts their set bits into a shared-memory list
 // with a warp prefix sum, then recomputes the listed lanes 32 at a time.
@@ -265,7 +391,8 @@ __global__ void __launch_bounds__(kBlock) k_math_probe(int op, int64_t n, const 
       case 3: r = invsqrt_f(x); break;
       case 4: r = hypot_big_f<false>(fabs_(x), fabs_(y), hard); break;
       case 5: r = scale_up(x, (int)y); break;
-      case 6: r = div_pos_big_f<false>(x, y, hard); break;
+      case 6: r = div_den<true>(x, make_den(y), hard); break;
+      case 9: r = div_pos_big_f<false>(x, y, hard); break;
       default: { double c, s; phase_f<false>(x, y, hypot_x(x, y), c, s, hard); r = (op == 7) ? c : s; } break;
     }
     o[i] = hard ? hard_marker() : r;
@@ -316,6 +443,13 @@ static Workspace& workspace(int dev) {
 
 constexpr int64_t kMaxLaunch = int64_t(1) << 31;     // lanes per sub-launch
 
+// Debug / A-B switches read once from the environment (e.g. B2S_NO_TMA=1
+// selects the register-prefetch streaming kernels).
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
+
 static int get_queue(int64_t n, HardQueue* q) {
   int dev = 0;
   B2S_CUDA(cudaGetDevice(&dev));
@@ -336,6 +470,34 @@ static int get_queue(int64_t n, HardQueue* q) {
   return 0;
 }
 
+static inline bool a16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static bool tma_ok_real(const RealArgs& A) {
+  if (getenv_flag("B2S_NO_TMA")) return false;
+  for (int t = 0; t < 4; t++) if (!a16(A.a[t])) return false;
+  return true;
+}
+
+static bool tma_ok_cplx(const CplxArgs& A) {
+  if (getenv_flag("B2S_NO_TMA")) return false;
+  for (int t = 0; t < 4; t++) if (!a16(A.ar[t]) || !a16(A.ai[t])) return false;
+  return true;
+}
+
+// Persistent grid: SMs x resident CTAs (registers and shared memory).
+template <typename K>
+static int tma_grid(K kernel, size_t smem, int64_t n) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t tiles = n / kBlock;
+  int64_t g = (int64_t)sms * per_sm;
+  if (tiles < g) g = tiles;
+  return g < 1 ? 1 : (int)g;
+}
+
 template <int Mode, bool Sine, bool States>
 static int launch_real(RealArgs A, cudaStream_t s) {
   const int64_t total = A.n;
@@ -351,8 +513,15 @@ static int launch_real(RealArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
-    auto k = k_svd2_real<Mode, Sine, States>;
-    k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
+    if (!States && tma_ok_real(A)) {
+      auto k = k_svd2_real_tma<Mode, Sine>;
+      const size_t sm = TmaRing<4>::kSmem;
+      B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
+    } else {
+      auto k = k_svd2_real<Mode, Sine, States>;
+      k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
+    }
     B2S_CUDA(cudaGetLastError());
     if (!States) {
       auto f = k_fix_real<Mode, Sine>;
@@ -380,8 +549,15 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
-    auto k = k_svd2_complex<Mode, Sine, States>;
-    k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
+    if (!States && tma_ok_cplx(A)) {
+      auto k = k_svd2_cplx_tma<Mode, Sine>;
+      const size_t sm = TmaRing<8>::kSmem;
+      B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
+    } else {
+      auto k = k_svd2_complex<Mode, Sine, States>;
+      k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
+    }
     B2S_CUDA(cudaGetLastError());
     if (!States) {
       auto f = k_fix_cplx<Mode, Sine>;
@@ -522,7 +698,7 @@ int b2s_backscale(int64_t n, const double* smax, const double* smin, const doubl
 }
 
 int b2s_math_probe(int op, int64_t n, const double* a, const double* b, double* out, void* stream) {
-  if (op < 0 || op > 8) return fail(1, "unknown probe op %d", op);
+  if (op < 0 || op > 9) return fail(1, "unknown probe op %d", op);
   if (n < 0) return fail(1, "negative n");
   if (!a || !out || ((op == 0 || op >= 4) && !b)) return fail(5, "NULL operand");
   if (n == 0) return 0;

@@ -95,18 +95,47 @@ def test_raw_quotient_in_range(gen):
 
 
 def test_checked_division_never_wrong(gen):
-    # 0 <= a <= b < 2^1023, including huge denominators and tiny numerators
-    for lo, hi, spread in ((1019, 1022, 60), (-50, 50, 60), (1000, 1022, 2100), (-1022, 1022, 2100)):
+    # 0 <= a <= b < 2^1024, including huge denominators and tiny numerators
+    for lo, hi, spread in ((1019, 1023, 60), (-50, 50, 60), (1000, 1023, 2100), (-1022, 1022, 2100)):
         b = rand_mag(N, lo, hi, gen)
         a = b * torch.rand(N, dtype=torch.float64, device=DEV, generator=gen) * torch.ldexp(
             torch.ones(N, dtype=torch.float64, device=DEV),
             -torch.randint(0, spread, (N,), device=DEV, generator=gen).to(torch.float64))
         a[:1000] = 0.0
-        q = probe(6, a, b)
+        q = probe(9, a, b)
         hard = bits(q) == HARD
         assert_same(q[~hard], (a / b)[~hard], "div_pos_big_f")
         if spread < 100:
             assert hard.float().mean().item() < 1e-3
+
+
+def test_normalised_division_full_range(gen):
+    """div_den: exact for every normal/zero numerator and normal denominator,
+    including subnormal and overflowing quotients; declines only subnormal
+    operands."""
+    sgn = lambda: torch.where(torch.rand(N, device=DEV, generator=gen) < 0.5, -1.0, 1.0).to(torch.float64)
+    for (la, ha), (lb, hb) in (((-1022, 1023), (-1022, 1023)), ((-1022, -900), (900, 1023)),
+                               ((1000, 1023), (-1022, -1000)), ((-60, 60), (-60, 60))):
+        a = rand_mag(N, la, ha, gen) * sgn()
+        b = rand_mag(N, lb, hb, gen) * sgn()
+        a[:1000] = 0.0
+        a[1000:2000] = -0.0
+        q = probe(6, a, b)
+        hard = bits(q) == HARD
+        assert not hard.any()
+        assert_same(q, a / b, "div_den [%d,%d]/[%d,%d]" % (la, ha, lb, hb))
+    # exact ties on the subnormal grid: d = D 2^1000 with a short mantissa D,
+    # a = D (2k+1) 2^-75 exactly, so a / d = (2k+1) 2^-1075 (a midpoint)
+    D = 1.0 + torch.randint(0, 1024, (N,), device=DEV, generator=gen).to(torch.float64) / 1024.0
+    k = torch.randint(0, 64, (N,), device=DEV, generator=gen).to(torch.float64)
+    d = D * 2.0 ** 1000
+    a = D * (2 * k + 1) * 2.0 ** -75
+    q = probe(6, a, d)
+    assert_same(q, a / d, "subnormal ties")
+    # subnormal operands are declined, never wrong
+    a = torch.full((4,), 5e-324, dtype=torch.float64, device=DEV)
+    b = torch.tensor([1.0, 2.0, 5e-324, 1e-310], dtype=torch.float64, device=DEV)
+    assert (bits(probe(6, a, b)) == HARD).all()
 
 
 def test_hypot_never_wrong(gen):

@@ -99,6 +99,25 @@ __device__ __forceinline__ double hypot_big_f(double m1, double m2, bool& hard) 
 // lanes.py:248-259 unit phase of re + i*im with mag = hypot(re, im) < 2^1023.
 // mag == 0 exactly when re == im == 0: then cos = +-1 (0/0 absorbed by the
 // relaxed min) and sin = im / TRUE_MIN = +-0.
+// Wide-exponent variant: quotients may be subnormal, so both use the
+// exponent-normalised division (exact for all normal operands).
+template <bool Fix>
+__device__ __forceinline__ void phase_w(double re, double im, double mag, double& c, double& s, bool& hard) {
+  const bool mz = !nz_(mag);
+  const Den D = make_den(mag);
+  bool hc = false, hs = false;
+  const double q1 = div_den(fabs_(re), D, hc);
+  const double q2 = div_den(im, D, hs);
+  c = or_(mz ? 1.0 : rmin(q1, 1.0), sgn_(re));
+  s = q2;
+  if (Fix) {
+    if (hc) c = or_(rmin(div_x(fabs_(re), mag), 1.0), sgn_(re));
+    if (hs) s = div_x(im, rmax(mag, kTrueMin()));
+  } else {
+    hard |= hc | hs;
+  }
+}
+
 template <bool Fix>
 __device__ __forceinline__ void phase_f(double re, double im, double mag, double& c, double& s, bool& hard) {
   const bool mz = !nz_(mag);
@@ -126,17 +145,27 @@ __device__ __forceinline__ void phase_f(double re, double im, double mag, double
 
 // svd2.py:306-343.  r11 = 0 or r11 in [2^1021, 2^1022.5] (the norm of the
 // pivot column, which holds the scaled maximum entry); 0 <= r12, r22 <= r11.
-template <bool Fix>
+template <bool Fix, bool Wide = false>
 __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bool& hard) {
-  // x = r12 / r11, y = r22 / r11 with one shared reciprocal of r11 / 4
-  // (r11 = 0 gives NaN quotients, absorbed to +0 exactly as the reference's
-  // 0/0 is).
-  const double b = mul(r11, 0.25);
-  const double r = rcp_f(b);
-  const double a12 = mul(r12, 0.25), a22 = mul(r22, 0.25);
-  double qx = quot_f(a12, b, r), qy = quot_f(a22, b, r);
-  const bool hx = nz_(r12) && !(resid_ok(hi_(a12)) && normal_q(hi_(qx)));
-  const bool hy = nz_(r22) && !(resid_ok(hi_(a22)) && normal_q(hi_(qy)));
+  double qx, qy;
+  bool hx = false, hy = false;
+  if (Wide) {
+    // exponent-normalised, exact for tiny ratios too (r11 = 0 only with
+    // r12 = r22 = 0, giving +0 like the reference's absorbed 0/0)
+    const Den D = make_den(r11);
+    qx = div_den(r12, D, hx);
+    qy = div_den(r22, D, hy);
+  } else {
+    // one shared reciprocal of r11 / 4 (r11 = 0 gives NaN quotients,
+    // absorbed to +0 exactly as the reference's 0/0 is)
+    const double b = mul(r11, 0.25);
+    const double r = rcp_f(b);
+    const double a12 = mul(r12, 0.25), a22 = mul(r22, 0.25);
+    qx = quot_f(a12, b, r);
+    qy = quot_f(a22, b, r);
+    hx = nz_(r12) && !(resid_ok(hi_(a12)) && normal_q(hi_(qx)));
+    hy = nz_(r22) && !(resid_ok(hi_(a22)) && normal_q(hi_(qy)));
+  }
   if (Fix) {
     if (hx) qx = div_fix(r12, r11);
     if (hy) qy = div_fix(r22, r11);
@@ -205,12 +234,31 @@ __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   return hard;
 }
 
+// A lane whose nonzero components span more than kWideSpread binades can
+// produce quotients below the normal range at the phase / rotation /
+// triangle sites; a warp holding any such lane runs the exponent-normalised
+// variant of those sites (warp-uniform, so no divergence).  The flag is only
+// a cost heuristic: either variant is exact wherever it does not set `hard`.
+constexpr int kWideSpread = 900;
+
+template <int N>
+__device__ __forceinline__ bool wide_lane(const double (&p)[N]) {
+  int emax = 0, emin = 0x7FF;
+  #pragma unroll
+  for (int i = 0; i < N; i++) {
+    const int e = (int)((hi_(p[i]) >> 20) & 0x7FFu);
+    emax = max(emax, e);
+    emin = min(emin, nz_(p[i]) ? e : 0x7FF);
+  }
+  return emax - emin > kWideSpread;
+}
+
 // ---------------------------------------------------------------------------
 // Complex lanes.  Scaled components are < 2^1022, so entry moduli are
 // < 2^1022.5; column norms, m11 and the rotated moduli r12, r22 stay below
 // 2^1023 and use the prescaling variants.
 // ---------------------------------------------------------------------------
-template <bool Sine, bool Fix>
+template <bool Sine, bool Fix, bool Wide = false>
 __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const double (&ai)[4], CplxOut& o) {
   bool hard = false;
   double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
@@ -236,25 +284,38 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
   swp(U.R, er[0], er[1]); swp(U.R, ei[0], ei[1]);
   swp(U.R, er[2], er[3]); swp(U.R, ei[2], ei[3]);
   swp(U.R, m11, m21);
-  phase_f<Fix>(er[0], ei[0], m11, U.c1, U.s1, hard);
-  phase_f<Fix>(er[1], ei[1], m21, U.c2, U.s2, hard);
+  if (Wide) {
+    phase_w<Fix>(er[0], ei[0], m11, U.c1, U.s1, hard);
+    phase_w<Fix>(er[1], ei[1], m21, U.c2, U.s2, hard);
+  } else {
+    phase_f<Fix>(er[0], ei[0], m11, U.c1, U.s1, hard);
+    phase_f<Fix>(er[1], ei[1], m21, U.c2, U.s2, hard);
+  }
   double f12r, f12i, f22r, f22i;
   cmul(U.c1, neg_(U.s1), er[2], ei[2], f12r, f12i);
   cmul(U.c2, neg_(U.s2), er[3], ei[3], f22r, f22i);
-  U.mt = div_pos_big_f<Fix>(m21, m11, hard);
+  if (Wide) {
+    bool h = false;
+    U.mt = div_den(m21, make_den(m11), h);           // m21 >= 0: relaxed_max is the identity
+    if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
+  } else {
+    U.mt = div_pos_big_f<Fix>(m21, m11, hard);
+  }
   U.cg = invsqrt_f(fma_(U.mt, U.mt, 1.0));
   const double g12r = mul(U.cg, fma_(U.mt, f22r, f12r)), g12i = mul(U.cg, fma_(U.mt, f22i, f12i));
   const double g22r = mul(U.cg, fnma_(U.mt, f12r, f22r)), g22i = mul(U.cg, fnma_(U.mt, f12i, f22i));
   const double r12 = hypot_big_f<Fix>(fabs_(g12r), fabs_(g12i), hard);
   double c12, s12;
-  phase_f<Fix>(g12r, g12i, r12, c12, s12, hard);
+  if (Wide) phase_w<Fix>(g12r, g12i, r12, c12, s12, hard);
+  else phase_f<Fix>(g12r, g12i, r12, c12, s12, hard);
   double wr, wi;
   cmul(c12, neg_(s12), g22r, g22i, wr, wi);
   const double r22 = hypot_big_f<Fix>(fabs_(wr), fabs_(wi), hard);
-  phase_f<Fix>(wr, wi, r22, U.dhr, U.dhi, hard);
+  if (Wide) phase_w<Fix>(wr, wi, r22, U.dhr, U.dhi, hard);
+  else phase_f<Fix>(wr, wi, r22, U.dhr, U.dhi, hard);
   U.dtr = c12;
   U.dti = neg_(s12);
-  const Tri T = triangle_f<Fix>(r11, r12, r22, hard);
+  const Tri T = triangle_f<Fix, Wide>(r11, r12, r22, hard);
   assemble_complex<Sine>(U, T, o);
   o.shift = shift;
   return hard;

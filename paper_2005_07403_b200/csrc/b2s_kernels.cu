@@ -118,7 +118,7 @@ __device__ __forceinline__ void redo_cplx(const CplxArgs& A, int64_t i) {
   #pragma unroll
   for (int t = 0; t < 4; t++) { ar[t] = A.ar[t][i]; ai[t] = A.ai[t][i]; }
   CplxOut o;
-  svd2_complex_f<Sine, true>(ar, ai, o);
+  svd2_complex_f<Sine, true, true>(ar, ai, o);
   store_cplx<Mode>(A, i, o);
 }
 
@@ -294,7 +294,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
     }
     const int64_t i = (blockIdx.x + k * gridDim.x) * kBlock + tid;
     CplxOut o;
-    const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
+    bool hard;
+    const double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
+    if (__any_sync(0xFFFFFFFFu, wide_lane<8>(p)))
+      hard = svd2_complex_f<Sine, false, true>(ar, ai, o);
+    else
+      hard = svd2_complex_f<Sine, false, false>(ar, ai, o);
     store_cplx<Mode>(A, i, o);
     mark_hard(A.q, hard, i);
   }

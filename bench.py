@@ -55,14 +55,18 @@ def peaks():
     return FALLBACK_HBM, "fallback"
 
 
-def ncu_traffic(config):
-    """Per-launch DRAM bytes from the committed ncu --set full summary."""
+def ncu_traffic(config, lanes):
+    """Per-launch DRAM bytes (read + write) of the streaming kernel and its
+    fix-up, from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, per lane) scaled to this launch's lanes."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
-        d = json.load(fh)
-    return d.get(str(config))
+        d = json.load(fh).get(str(config))
+    if not d:
+        return None
+    return round(d["bytes_per_lane"] * lanes)
 
 
 class Clocks:
@@ -204,9 +208,10 @@ def run_device(config, world, rank, local, steps, warmup):
     avg_kernel_ms = max_over_ranks(float(np.mean(kern_ms)), world)
     del re, im, out, outd, in_re, in_im
     torch.cuda.empty_cache()
+    # per step: the streaming kernel + the hard-lane fix-up kernel
     return {"n_total": n_total, "n_shard": n, "field": field,
             "total_ms": total_ms, "avg_kernel_ms": avg_kernel_ms,
-            "clocks": clk, "launches": steps}
+            "clocks": clk, "launches": 2 * steps}
 
 
 def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
@@ -257,7 +262,7 @@ def roofline(res, config, hbm, how):
     field = res["field"]
     bytes_per_launch = BYTES_PER_SVD[field] * res["n_shard"]
     achieved = bytes_per_launch / (res["avg_kernel_ms"] * 1e-3) / 1e9
-    traffic = ncu_traffic(config)
+    traffic = ncu_traffic(config, res["n_shard"])
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
             "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_source": how,
             "traffic": traffic,

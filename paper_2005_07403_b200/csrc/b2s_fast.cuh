@@ -104,10 +104,10 @@ __device__ __forceinline__ double hypot_big_f(double m1, double m2, bool& hard) 
 template <bool Fix>
 __device__ __forceinline__ void phase_w(double re, double im, double mag, double& c, double& s, bool& hard) {
   const bool mz = !nz_(mag);
-  const Den D = make_den(mag);
+  const Den D = make_den<Fix>(mag);
   bool hc = false, hs = false;
-  const double q1 = div_den(fabs_(re), D, hc);
-  const double q2 = div_den(im, D, hs);
+  const double q1 = div_den<false, Fix>(fabs_(re), D, hc);
+  const double q2 = div_den<false, Fix>(im, D, hs);
   c = or_(mz ? 1.0 : rmin(q1, 1.0), sgn_(re));
   s = q2;
   if (Fix) {
@@ -152,9 +152,9 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   if (Wide) {
     // exponent-normalised, exact for tiny ratios too (r11 = 0 only with
     // r12 = r22 = 0, giving +0 like the reference's absorbed 0/0)
-    const Den D = make_den(r11);
-    qx = div_den(r12, D, hx);
-    qy = div_den(r22, D, hy);
+    const Den D = make_den<Fix>(r11);
+    qx = div_den<false, Fix>(r12, D, hx);
+    qy = div_den<false, Fix>(r22, D, hy);
   } else {
     // one shared reciprocal of r11 / 4 (r11 = 0 gives NaN quotients,
     // absorbed to +0 exactly as the reference's 0/0 is)
@@ -178,6 +178,8 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   const double num = mul(mul(lo, 2.0), hi);                  // scalef(min, 1) * max
   const double den = fma_(sub(x, y), add(x, y), 1.0);         // in [0, 2]
   // num / den: num == 0 gives +0 or NaN (den == 0), both absorbed to +0.
+  // (Cheap in both variants: it flags ~0.6% of config-4 lanes, cheaper to
+  // fix than to normalise for every wide warp.)
   double qn = quot_f(num, den, rcp_f(den));
   const bool hn = nz_(num) && !(resid_ok(hi_(num)) && normal_q(hi_(qn)));
   if (Fix) { if (hn) qn = div_fix(num, den); } else hard |= hn;
@@ -296,7 +298,7 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
   cmul(U.c2, neg_(U.s2), er[3], ei[3], f22r, f22i);
   if (Wide) {
     bool h = false;
-    U.mt = div_den(m21, make_den(m11), h);           // m21 >= 0: relaxed_max is the identity
+    U.mt = div_den<false, Fix>(m21, make_den<Fix>(m11), h);   // m21 >= 0: relaxed_max is the identity
     if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
   } else {
     U.mt = div_pos_big_f<Fix>(m21, m11, hard);

@@ -124,14 +124,23 @@ __device__ __forceinline__ void redo_cplx(const CplxArgs& A, int64_t i) {
 
 // Record this warp's hard lanes: one ballot word per 32 consecutive lanes.
 // Lane 0 of the warp always holds the lowest (32-aligned) index.
-__device__ __forceinline__ void mark_hard(const HardQueue& q, bool hard, int64_t i) {
+// Returns the number of hard lanes in the word (meaningful on lane 0).
+__device__ __forceinline__ unsigned mark_hard(const HardQueue& q, bool hard, int64_t i) {
   const unsigned m = __ballot_sync(__activemask(), hard);
   if ((threadIdx.x & 31) == 0) q.mask[i >> 5] = m;
+  return (unsigned)__popc(m);
+}
+
+// One atomic per warp at kernel end: the launch's hard-lane total, which
+// the fix-up kernel checks before scanning the mask.
+__device__ __forceinline__ void count_hard(const HardQueue& q, unsigned long long n) {
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(q.cnt, n);
 }
 
 template <int Mode, bool Sine, bool States>
 __global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
+  unsigned long long nh = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= A.n) return;
   double nx[4];
@@ -153,14 +162,16 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
     } else {
       const bool hard = svd2_real_f<Sine, false>(a, o);
       store_real<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
-      mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i);
     }
   }
+  count_hard(A.q, nh);
 }
 
 template <int Mode, bool Sine, bool States>
 __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
+  unsigned long long nh = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= A.n) return;
   double nr[4], ni[4];
@@ -183,9 +194,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
     } else {
       const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
       store_cplx<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
-      mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i);
     }
   }
+  count_hard(A.q, nh);
 }
 
 // ---------------------------------------------------------------------------
@@ -235,6 +247,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
   TmaRing<4> R;
   R.init(smem);
   const int tid = threadIdx.x;
+  unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0)
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
     RealOut o;
     const bool hard = svd2_real_f<Sine, false>(a, o);
     store_real<Mode>(A, i, o);
-    mark_hard(A.q, hard, i);
+    nh += mark_hard(A.q, hard, i);
   }
   if (blockIdx.x == 0) {
     const int64_t i = tiles * kBlock + tid;
@@ -265,9 +278,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
       RealOut o;
       const bool hard = svd2_real_f<Sine, false>(a, o);
       store_real<Mode>(A, i, o);
-      mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i);
     }
   }
+  count_hard(A.q, nh);
 }
 
 template <int Mode, bool Sine>
@@ -277,6 +291,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
   R.init(smem);
   const double* src[8] = {A.ar[0], A.ar[1], A.ar[2], A.ar[3], A.ai[0], A.ai[1], A.ai[2], A.ai[3]};
   const int tid = threadIdx.x;
+  unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0)
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
     else
       hard = svd2_complex_f<Sine, false, false>(ar, ai, o);
     store_cplx<Mode>(A, i, o);
-    mark_hard(A.q, hard, i);
+    nh += mark_hard(A.q, hard, i);
   }
   if (blockIdx.x == 0) {
     const int64_t i = tiles * kBlock + tid;
@@ -312,9 +327,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
       CplxOut o;
       const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
       store_cplx<Mode>(A, i, o);
-      mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i);
     }
   }
+  count_hard(A.q, nh);
 }
 
 // Exact fix-up of the marked hard lanes.  Each warp takes 32 mask words
@@ -325,10 +341,10 @@ constexpr int kFixWarps = kBlock / 32;
 template <typename Redo>
 __device__ __forceinline__ void fix_lanes(const HardQueue& q, int64_t n, Redo redo) {
   __shared__ unsigned list[kFixWarps][1024];
+  if (*q.cnt == 0ull) return;               // the streaming kernel found no hard lane
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t words = (n + 31) >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * kFixWarps;
-  unsigned long long found = 0;
   for (int64_t base = ((int64_t)blockIdx.x * kFixWarps + warp) * 32; base < words; base += nwarps * 32) {
     const unsigned w = (base + lane < words) ? q.mask[base + lane] : 0u;
     const int c = __popc(w);
@@ -350,9 +366,7 @@ __device__ __forceinline__ void fix_lanes(const HardQueue& q, int64_t n, Redo re
     __syncwarp();
     for (int j = lane; j < total; j += 32) redo((int64_t)list[warp][j]);
     __syncwarp();
-    found += (unsigned long long)total;
   }
-  if (lane == 0 && found) atomicAdd(q.cnt, found);
 }
 
 template <int Mode, bool Sine>

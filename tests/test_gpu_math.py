@@ -132,10 +132,15 @@ def test_normalised_division_full_range(gen):
     a = D * (2 * k + 1) * 2.0 ** -75
     q = probe(6, a, d)
     assert_same(q, a / d, "subnormal ties")
-    # subnormal operands are declined, never wrong
-    a = torch.full((4,), 5e-324, dtype=torch.float64, device=DEV)
-    b = torch.tensor([1.0, 2.0, 5e-324, 1e-310], dtype=torch.float64, device=DEV)
-    assert (bits(probe(6, a, b)) == HARD).all()
+    # subnormal operands are normalised exactly
+    a = rand_mag(N, -1074, -1023, gen) * sgn()
+    b = rand_mag(N, -1074, 1023, gen) * sgn()
+    q = probe(6, a, b)
+    assert_same(q, a / b, "div_den subnormal operands")
+    assert_same(probe(6, b, a), b / a, "div_den subnormal denominators")
+    # zero denominators are declined
+    z = torch.zeros(4, dtype=torch.float64, device=DEV)
+    assert (bits(probe(6, a[:4], z)) == HARD).all()
 
 
 def test_hypot_never_wrong(gen):

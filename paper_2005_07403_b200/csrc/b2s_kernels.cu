@@ -125,8 +125,13 @@ __device__ __forceinline__ void redo_cplx(const CplxArgs& A, int64_t i) {
 // Record this warp's hard lanes: one ballot word per 32 consecutive lanes.
 // Lane 0 of the warp always holds the lowest (32-aligned) index.
 // Returns the number of hard lanes in the word (meaningful on lane 0).
-__device__ __forceinline__ unsigned mark_hard(const HardQueue& q, bool hard, int64_t i) {
-  const unsigned m = __ballot_sync(__activemask(), hard);
+// `members` must name every lane of the warp that holds a lane of this
+// 32-lane word: the full mask inside the TMA tile loops (which also forces
+// warp 0 to reconverge after thread 0's producer work), the active mask in
+// the grid-stride and tail loops.
+__device__ __forceinline__ unsigned mark_hard(const HardQueue& q, bool hard, int64_t i,
+                                              unsigned members = 0xFFFFFFFFu) {
+  const unsigned m = __ballot_sync(members, hard);
   if ((threadIdx.x & 31) == 0) q.mask[i >> 5] = m;
   return (unsigned)__popc(m);
 }
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
     } else {
       const bool hard = svd2_real_f<Sine, false>(a, o);
       store_real<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
-      nh += mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i, __activemask());
     }
   }
   count_hard(A.q, nh);
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
     } else {
       const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
       store_cplx<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
-      nh += mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i, __activemask());
     }
   }
   count_hard(A.q, nh);
@@ -211,59 +216,100 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // CTA 0 with ordinary loads.
 // ---------------------------------------------------------------------------
 constexpr int kStages = 4;
+constexpr int kWarps = kBlock / 32;
 
+// Force the loaded values into registers (scoreboard wait) before what
+// follows in program order.
+__device__ __forceinline__ void consumed(const double (&v)[4]) {
+  asm volatile("" ::"d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]) : "memory");
+}
+
+// Producer/consumer ring without CTA barriers.  full[s] (an mbarrier)
+// completes when the bulk copies of a tile land (one arrive.expect_tx plus
+// the TMA transaction bytes).  Stage release is a shared counter: each warp,
+// once its loads from the stage have landed (`consumed`), increments it, and
+// the warp that brings it to kWarps -- the last reader -- resets it and
+// issues the refill of that stage with the CTA's tile kStages ahead.  No
+// warp ever waits for another except on data, and no thread polls.
 template <int NT>
 struct TmaRing {
   static constexpr uint32_t kTileBytes = kBlock * sizeof(double);
-  static constexpr size_t kSmem = (size_t)kStages * NT * kBlock * sizeof(double) + kStages * sizeof(uint64_t);
+  static constexpr size_t kBuf = (size_t)kStages * NT * kBlock * sizeof(double);
+  static constexpr size_t kSmem = kBuf + kStages * (sizeof(uint64_t) + sizeof(int));
   double* buf;      // [kStages][NT][kBlock]
-  uint64_t* bar;    // [kStages]
-  uint64_t pol;
+  uint64_t* full;   // [kStages]
+  int* readers;     // [kStages]
+  const double* const* src;
+  int64_t mine;
 
   __device__ __forceinline__ double* stage(int s, int t) { return buf + ((size_t)s * NT + t) * kBlock; }
+  __device__ __forceinline__ int64_t tile(int64_t j) const { return blockIdx.x + j * gridDim.x; }
 
-  __device__ __forceinline__ void init(char* smem) {
+  __device__ __forceinline__ void init(char* smem, const double* const* src_, int64_t mine_) {
     buf = reinterpret_cast<double*>(smem);
-    bar = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * NT * kBlock * sizeof(double));
+    full = reinterpret_cast<uint64_t*>(smem + kBuf);
+    readers = reinterpret_cast<int*>(full + kStages);
+    src = src_;
+    mine = mine_;
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kStages; s++) tma::mbar_init(&bar[s], 1);
+      for (int s = 0; s < kStages; s++) {
+        tma::mbar_init(&full[s], 1);
+        readers[s] = 0;
+      }
       tma::fence_init();
     }
     __syncthreads();
-    pol = threadIdx.x == 0 ? tma::evict_first_policy() : 0;
+    if (threadIdx.x == 0)
+      for (int64_t j = 0; j < kStages && j < mine; j++) issue((int)j, tile(j));
   }
 
-  // thread 0 only: fill stage s with tile `tile` of the NT trains src[]
-  __device__ __forceinline__ void issue(int s, const double* const* src, int64_t tile) {
-    tma::mbar_arrive_expect_tx(&bar[s], NT * kTileBytes);
+  __device__ __forceinline__ void issue(int s, int64_t t) {
+    const uint64_t pol = tma::evict_first_policy();
+    tma::mbar_arrive_expect_tx(&full[s], NT * kTileBytes);
     #pragma unroll
-    for (int t = 0; t < NT; t++) tma::bulk_load(stage(s, t), src[t] + tile * kBlock, kTileBytes, &bar[s], pol);
+    for (int k = 0; k < NT; k++) tma::bulk_load(stage(s, k), src[k] + t * kBlock, kTileBytes, &full[s], pol);
+  }
+
+  __device__ __forceinline__ void wait_full(int64_t j) {
+    tma::mbar_wait(&full[(int)(j % kStages)], (uint32_t)((j / kStages) & 1));
+  }
+
+  __device__ __forceinline__ void release(int64_t j) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const int s = (int)(j % kStages);
+      __threadfence_block();                               // release this warp's reads
+      if (atomicAdd(&readers[s], 1) == kWarps - 1) {
+        __threadfence_block();                             // acquire the other warps' reads
+        readers[s] = 0;
+        if (j + kStages < mine) {
+          tma::fence_proxy_async();
+          issue(s, tile(j + kStages));
+        }
+      }
+    }
   }
 };
 
 template <int Mode, bool Sine>
 __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
   extern __shared__ __align__(128) char smem[];
-  TmaRing<4> R;
-  R.init(smem);
   const int tid = threadIdx.x;
   unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (tid == 0)
-    for (int s = 0; s < kStages && s < mine; s++) R.issue(s, A.a, blockIdx.x + (int64_t)s * gridDim.x);
+  const double* src[4] = {A.a[0], A.a[1], A.a[2], A.a[3]};
+  TmaRing<4> R;
+  R.init(smem, src, mine);
   for (int64_t k = 0; k < mine; k++) {
     const int s = (int)(k % kStages);
-    tma::mbar_wait(&R.bar[s], (uint32_t)((k / kStages) & 1));
+    R.wait_full(k);
     double a[4];
     #pragma unroll
     for (int t = 0; t < 4; t++) a[t] = R.stage(s, t)[tid];
-    __syncthreads();                       // every thread has read stage s
-    if (tid == 0 && k + kStages < mine) {
-      tma::fence_proxy_async();
-      R.issue(s, A.a, blockIdx.x + (k + kStages) * gridDim.x);
-    }
-    const int64_t i = (blockIdx.x + k * gridDim.x) * kBlock + tid;
+    consumed(a);
+    R.release(k);
+    const int64_t i = R.tile(k) * kBlock + tid;
     RealOut o;
     const bool hard = svd2_real_f<Sine, false>(a, o);
     store_real<Mode>(A, i, o);
@@ -278,36 +324,32 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
       RealOut o;
       const bool hard = svd2_real_f<Sine, false>(a, o);
       store_real<Mode>(A, i, o);
-      nh += mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i, __activemask());
     }
   }
   count_hard(A.q, nh);
 }
 
 template <int Mode, bool Sine>
-__global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
+__global__ void __launch_bounds__(kBlock, 3) k_svd2_cplx_tma(const CplxArgs A) {
   extern __shared__ __align__(128) char smem[];
-  TmaRing<8> R;
-  R.init(smem);
   const double* src[8] = {A.ar[0], A.ar[1], A.ar[2], A.ar[3], A.ai[0], A.ai[1], A.ai[2], A.ai[3]};
   const int tid = threadIdx.x;
   unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (tid == 0)
-    for (int s = 0; s < kStages && s < mine; s++) R.issue(s, src, blockIdx.x + (int64_t)s * gridDim.x);
+  TmaRing<8> R;
+  R.init(smem, src, mine);
   for (int64_t k = 0; k < mine; k++) {
     const int s = (int)(k % kStages);
-    tma::mbar_wait(&R.bar[s], (uint32_t)((k / kStages) & 1));
+    R.wait_full(k);
     double ar[4], ai[4];
     #pragma unroll
     for (int t = 0; t < 4; t++) { ar[t] = R.stage(s, t)[tid]; ai[t] = R.stage(s, 4 + t)[tid]; }
-    __syncthreads();
-    if (tid == 0 && k + kStages < mine) {
-      tma::fence_proxy_async();
-      R.issue(s, src, blockIdx.x + (k + kStages) * gridDim.x);
-    }
-    const int64_t i = (blockIdx.x + k * gridDim.x) * kBlock + tid;
+    consumed(ar);
+    consumed(ai);
+    R.release(k);
+    const int64_t i = R.tile(k) * kBlock + tid;
     CplxOut o;
     bool hard;
     const double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
@@ -327,10 +369,41 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_cplx_tma(const CplxArgs A) {
       CplxOut o;
       const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
       store_cplx<Mode>(A, i, o);
-      nh += mark_hard(A.q, hard, i);
+      nh += mark_hard(A.q, hard, i, __activemask());
     }
   }
   count_hard(A.q, nh);
+}
+
+// Diagnostic: stream 4 trains through the TMA ring unchanged (tests the
+// ring protocol in isolation; `spin` adds per-lane busy work so warps drift
+// apart).
+__global__ void __launch_bounds__(kBlock, 4) k_ring_probe(const RealArgs A, int spin) {
+  extern __shared__ __align__(128) char smem[];
+  const double* src[4] = {A.a[0], A.a[1], A.a[2], A.a[3]};
+  const int tid = threadIdx.x;
+  const int64_t tiles = A.n / kBlock;
+  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  TmaRing<4> R;
+  R.init(smem, src, mine);
+  for (int64_t k = 0; k < mine; k++) {
+    const int s = (int)(k % kStages);
+    R.wait_full(k);
+    double a[4];
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = R.stage(s, t)[tid];
+    consumed(a);
+    R.release(k);
+    const int64_t i = R.tile(k) * kBlock + tid;
+    double x = a[0];
+    const int w = tid >> 5;
+    const int reps = spin >= 0 ? spin * (w + 1) : -spin * (kWarps - w) * (1 + (int)((i * 2654435761u) >> 28 & 3));
+    for (int r = 0; r < reps; r++) x = __fma_rn(x, 1.0, 0.0);
+    A.u[0][i] = x;
+    A.u[1][i] = a[1];
+    A.u[2][i] = a[2];
+    A.u[3][i] = a[3];
+  }
 }
 
 // Exact fix-up of the marked hard lanes.  Each warp takes 32 mask words
@@ -756,6 +829,17 @@ long long b2s_hard_lane_count(int device) {
   }
   cudaSetDevice(prev);
   return out;
+}
+
+int b2s_ring_probe(int64_t n, const double* const a[4], double* const out[4], int spin, void* stream) {
+  RealArgs A{};
+  A.n = n;
+  for (int t = 0; t < 4; t++) { A.a[t] = a[t]; A.u[t] = out[t]; }
+  const size_t sm = TmaRing<4>::kSmem;
+  B2S_CUDA(cudaFuncSetAttribute(k_ring_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_ring_probe<<<tma_grid(k_ring_probe, sm, n), kBlock, sm, (cudaStream_t)stream>>>(A, spin);
+  B2S_CUDA(cudaGetLastError());
+  return 0;
 }
 
 int b2s_check_fp_env(int device) {

@@ -79,6 +79,28 @@ int b2s_svd2_complex(int64_t n, const double *const a_re[4],
                      double *const *states, void *stream);
 
 /*
+ * AoSoA-8 record input (the reference's on-disk test-file layout,
+ * cli.py:102-134): matrix k is lane k % 8 of record
+ * k / 8; a real record is 4 consecutive 8-lane vectors e11, e21, e12, e22
+ * (256 B), a complex record 8 vectors with re/im interleaved per entry
+ * (e11re, e11im, e21re, ...; 512 B).  The kernels read the records
+ * directly (a 256-lane tile is one contiguous block of 32 records fetched
+ * by the TMA ring), with no repack pass; outputs are SoA trains as for
+ * b2s_svd2_real / _complex.  `records` (device, 16-byte aligned) must hold
+ * ceil(n / 8) records.
+ */
+int b2s_svd2_real_records(int64_t n, const double *records, double *const u[4],
+                          double *const v[4], double *smax, double *smin,
+                          double *shift, int backscale_mode, int flags,
+                          void *stream);
+
+int b2s_svd2_complex_records(int64_t n, const double *records,
+                             double *const u_re[4], double *const u_im[4],
+                             double *const v_re[4], double *const v_im[4],
+                             double *smax, double *smin, double *shift,
+                             int backscale_mode, int flags, void *stream);
+
+/*
  * Host-buffer variants: the reference-facing call a ctypes/cffi binding of
  * driver.run_batch (driver.py:149-190) makes with numpy trains.  Inputs and
  * outputs are HOST pointers (pinned memory gives full PCIe overlap); the

@@ -33,6 +33,7 @@ struct HardQueue {
 
 struct RealArgs {
   HardQueue q;
+  int aos;        // 1: a[0] points at AoSoA-8 records (cli.py:102-134 layout)
   int64_t n;
   const double* a[4];
   double* u[4];
@@ -43,6 +44,7 @@ struct RealArgs {
 
 struct CplxArgs {
   HardQueue q;
+  int aos;        // 1: ar[0] points at AoSoA-8 complex records
   int64_t n;
   const double* ar[4];
   const double* ai[4];
@@ -101,12 +103,36 @@ __device__ __forceinline__ void store_cplx(const CplxArgs& A, int64_t i, CplxOut
   st_stream(A.shift + i, o.shift);
 }
 
+// Lane i's inputs from SoA trains, or from AoSoA-8 records: matrix i is lane
+// i % 8 of record i / 8; a real record holds the 8-lane vectors e11, e21,
+// e12, e22, a complex one e11re, e11im, e21re, ... (cli.py:102-134).
+__device__ __forceinline__ void load_real(const RealArgs& A, int64_t i, double (&a)[4]) {
+  if (A.aos) {
+    const double* r = A.a[0] + (i >> 3) * 32 + (i & 7);
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = r[8 * t];
+  } else {
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = A.a[t][i];
+  }
+}
+
+__device__ __forceinline__ void load_cplx(const CplxArgs& A, int64_t i, double (&ar)[4], double (&ai)[4]) {
+  if (A.aos) {
+    const double* r = A.ar[0] + (i >> 3) * 64 + (i & 7);
+    #pragma unroll
+    for (int t = 0; t < 4; t++) { ar[t] = r[16 * t]; ai[t] = r[16 * t + 8]; }
+  } else {
+    #pragma unroll
+    for (int t = 0; t < 4; t++) { ar[t] = A.ar[t][i]; ai[t] = A.ai[t][i]; }
+  }
+}
+
 // A marked lane again, with every failing call site re-evaluated exactly.
 template <int Mode, bool Sine>
 __device__ __forceinline__ void redo_real(const RealArgs& A, int64_t i) {
   double a[4];
-  #pragma unroll
-  for (int t = 0; t < 4; t++) a[t] = A.a[t][i];
+  load_real(A, i, a);
   RealOut o;
   svd2_real_f<Sine, true>(a, o);
   store_real<Mode>(A, i, o);
@@ -115,8 +141,7 @@ __device__ __forceinline__ void redo_real(const RealArgs& A, int64_t i) {
 template <int Mode, bool Sine>
 __device__ __forceinline__ void redo_cplx(const CplxArgs& A, int64_t i) {
   double ar[4], ai[4];
-  #pragma unroll
-  for (int t = 0; t < 4; t++) { ar[t] = A.ar[t][i]; ai[t] = A.ai[t][i]; }
+  load_cplx(A, i, ar, ai);
   CplxOut o;
   svd2_complex_f<Sine, true, true>(ar, ai, o);
   store_cplx<Mode>(A, i, o);
@@ -241,16 +266,19 @@ struct TmaRing {
   int* readers;     // [kStages]
   const double* const* src;
   int64_t mine;
+  int64_t tstride;    // elements between consecutive tiles of one source
 
   __device__ __forceinline__ double* stage(int s, int t) { return buf + ((size_t)s * NT + t) * kBlock; }
   __device__ __forceinline__ int64_t tile(int64_t j) const { return blockIdx.x + j * gridDim.x; }
 
-  __device__ __forceinline__ void init(char* smem, const double* const* src_, int64_t mine_) {
+  __device__ __forceinline__ void init(char* smem, const double* const* src_, int64_t mine_,
+                                      int64_t tstride_ = kBlock) {
     buf = reinterpret_cast<double*>(smem);
     full = reinterpret_cast<uint64_t*>(smem + kBuf);
     readers = reinterpret_cast<int*>(full + kStages);
     src = src_;
     mine = mine_;
+    tstride = tstride_;
     if (threadIdx.x == 0) {
       for (int s = 0; s < kStages; s++) {
         tma::mbar_init(&full[s], 1);
@@ -267,7 +295,7 @@ struct TmaRing {
     const uint64_t pol = tma::evict_first_policy();
     tma::mbar_arrive_expect_tx(&full[s], NT * kTileBytes);
     #pragma unroll
-    for (int k = 0; k < NT; k++) tma::bulk_load(stage(s, k), src[k] + t * kBlock, kTileBytes, &full[s], pol);
+    for (int k = 0; k < NT; k++) tma::bulk_load(stage(s, k), src[k] + t * tstride, kTileBytes, &full[s], pol);
   }
 
   __device__ __forceinline__ void wait_full(int64_t j) {
@@ -291,22 +319,34 @@ struct TmaRing {
   }
 };
 
-template <int Mode, bool Sine>
+// AoS = true: the source is AoSoA-8 records; a 256-lane tile is one
+// contiguous 8 KiB (real) / 16 KiB (complex) block of 32 records, fetched by
+// the same NT 2 KiB bulk copies, and each thread picks its lane's components
+// out of the record layout in shared memory (no separate repack pass).
+template <int NT, bool AoS>
+__device__ __forceinline__ double stage_val(double* st0, int v, int tid) {
+  if (AoS) return st0[(tid >> 3) * (NT * 8) + v * 8 + (tid & 7)];
+  return st0[v * kBlock + tid];
+}
+
+template <int Mode, bool Sine, bool AoS>
 __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
   extern __shared__ __align__(128) char smem[];
+  const double* src[4];
+  #pragma unroll
+  for (int t = 0; t < 4; t++) src[t] = AoS ? A.a[0] + t * kBlock : A.a[t];
   const int tid = threadIdx.x;
   unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const double* src[4] = {A.a[0], A.a[1], A.a[2], A.a[3]};
   TmaRing<4> R;
-  R.init(smem, src, mine);
+  R.init(smem, src, mine, AoS ? 4 * kBlock : kBlock);
   for (int64_t k = 0; k < mine; k++) {
     const int s = (int)(k % kStages);
     R.wait_full(k);
     double a[4];
     #pragma unroll
-    for (int t = 0; t < 4; t++) a[t] = R.stage(s, t)[tid];
+    for (int t = 0; t < 4; t++) a[t] = stage_val<4, AoS>(R.stage(s, 0), t, tid);
     consumed(a);
     R.release(k);
     const int64_t i = R.tile(k) * kBlock + tid;
@@ -319,8 +359,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
     const int64_t i = tiles * kBlock + tid;
     if (i < A.n) {
       double a[4];
-      #pragma unroll
-      for (int t = 0; t < 4; t++) a[t] = A.a[t][i];
+      load_real(A, i, a);
       RealOut o;
       const bool hard = svd2_real_f<Sine, false>(a, o);
       store_real<Mode>(A, i, o);
@@ -330,22 +369,31 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
   count_hard(A.q, nh);
 }
 
-template <int Mode, bool Sine>
+template <int Mode, bool Sine, bool AoS>
 __global__ void __launch_bounds__(kBlock, 3) k_svd2_cplx_tma(const CplxArgs A) {
   extern __shared__ __align__(128) char smem[];
-  const double* src[8] = {A.ar[0], A.ar[1], A.ar[2], A.ar[3], A.ai[0], A.ai[1], A.ai[2], A.ai[3]};
+  const double* src[8];
+  #pragma unroll
+  for (int t = 0; t < 4; t++) {
+    src[t] = AoS ? A.ar[0] + t * kBlock : A.ar[t];
+    src[4 + t] = AoS ? A.ar[0] + (4 + t) * kBlock : A.ai[t];
+  }
   const int tid = threadIdx.x;
   unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   TmaRing<8> R;
-  R.init(smem, src, mine);
+  R.init(smem, src, mine, AoS ? 8 * kBlock : kBlock);
   for (int64_t k = 0; k < mine; k++) {
     const int s = (int)(k % kStages);
     R.wait_full(k);
     double ar[4], ai[4];
     #pragma unroll
-    for (int t = 0; t < 4; t++) { ar[t] = R.stage(s, t)[tid]; ai[t] = R.stage(s, 4 + t)[tid]; }
+    for (int t = 0; t < 4; t++) {
+      // SoA stage order: re trains then im trains; record order: re/im per entry
+      ar[t] = stage_val<8, AoS>(R.stage(s, 0), AoS ? 2 * t : t, tid);
+      ai[t] = stage_val<8, AoS>(R.stage(s, 0), AoS ? 2 * t + 1 : 4 + t, tid);
+    }
     consumed(ar);
     consumed(ai);
     R.release(k);
@@ -364,8 +412,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_cplx_tma(const CplxArgs A) {
     const int64_t i = tiles * kBlock + tid;
     if (i < A.n) {
       double ar[4], ai[4];
-      #pragma unroll
-      for (int t = 0; t < 4; t++) { ar[t] = A.ar[t][i]; ai[t] = A.ai[t][i]; }
+      load_cplx(A, i, ar, ai);
       CplxOut o;
       const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
       store_cplx<Mode>(A, i, o);
@@ -597,7 +644,9 @@ static int launch_real(RealArgs A, cudaStream_t s) {
   for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
     A = base;
     A.n = (total - lo) < kMaxLaunch ? (total - lo) : kMaxLaunch;
-    for (int t = 0; t < 4; t++) { A.a[t] += lo; A.u[t] += lo; A.v[t] += lo; }
+    for (int t = 0; t < 4; t++) { A.u[t] += lo; A.v[t] += lo; }
+    if (A.aos) A.a[0] += lo * 4;                 // 32 doubles per 8 lanes
+    else for (int t = 0; t < 4; t++) A.a[t] += lo;
     A.smax += lo; A.smin += lo; A.shift += lo;
     if (States) for (int k = 0; k < B2S_STATES_REAL; k++) A.st[k] += lo;
     if (!States) {
@@ -605,8 +654,8 @@ static int launch_real(RealArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
-    if (!States && tma_ok_real(A)) {
-      auto k = k_svd2_real_tma<Mode, Sine>;
+    if (!States && (A.aos || tma_ok_real(A))) {
+      auto k = A.aos ? k_svd2_real_tma<Mode, Sine, true> : k_svd2_real_tma<Mode, Sine, false>;
       const size_t sm = TmaRing<4>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
@@ -631,9 +680,9 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
   for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
     A = base;
     A.n = (total - lo) < kMaxLaunch ? (total - lo) : kMaxLaunch;
-    for (int t = 0; t < 4; t++) {
-      A.ar[t] += lo; A.ai[t] += lo; A.ur[t] += lo; A.ui[t] += lo; A.vr[t] += lo; A.vi[t] += lo;
-    }
+    for (int t = 0; t < 4; t++) { A.ur[t] += lo; A.ui[t] += lo; A.vr[t] += lo; A.vi[t] += lo; }
+    if (A.aos) A.ar[0] += lo * 8;                // 64 doubles per 8 lanes
+    else for (int t = 0; t < 4; t++) { A.ar[t] += lo; A.ai[t] += lo; }
     A.smax += lo; A.smin += lo; A.shift += lo;
     if (States) for (int k = 0; k < B2S_STATES_COMPLEX; k++) A.st[k] += lo;
     if (!States) {
@@ -641,8 +690,8 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
-    if (!States && tma_ok_cplx(A)) {
-      auto k = k_svd2_cplx_tma<Mode, Sine>;
+    if (!States && (A.aos || tma_ok_cplx(A))) {
+      auto k = A.aos ? k_svd2_cplx_tma<Mode, Sine, true> : k_svd2_cplx_tma<Mode, Sine, false>;
       const size_t sm = TmaRing<8>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
@@ -697,12 +746,14 @@ static int check_common(int64_t n, int mode, int flags, double* const* states) {
   } while (0)
 
 int real_entry(int64_t n, const double* const a[4], double* const u[4], double* const v[4], double* smax,
-               double* smin, double* shift, int mode, int flags, double* const* states, cudaStream_t s) {
+               double* smin, double* shift, int mode, int flags, double* const* states, cudaStream_t s,
+               int aos = 0) {
   int rc = check_common(n, mode, flags, states);
   if (rc) return rc;
   if (!a || !u || !v) return fail(5, "train pointer array is NULL");
   RealArgs A{};
   A.n = n;
+  A.aos = aos;
   for (int t = 0; t < 4; t++) {
     B2S_CHECK_PTR(a[t], "input train");
     B2S_CHECK_PTR(u[t], "u train");
@@ -721,12 +772,13 @@ int real_entry(int64_t n, const double* const a[4], double* const u[4], double* 
 
 int cplx_entry(int64_t n, const double* const ar[4], const double* const ai[4], double* const ur[4],
                double* const ui[4], double* const vr[4], double* const vi[4], double* smax, double* smin,
-               double* shift, int mode, int flags, double* const* states, cudaStream_t s) {
+               double* shift, int mode, int flags, double* const* states, cudaStream_t s, int aos = 0) {
   int rc = check_common(n, mode, flags, states);
   if (rc) return rc;
   if (!ar || !ai || !ur || !ui || !vr || !vi) return fail(5, "train pointer array is NULL");
   CplxArgs A{};
   A.n = n;
+  A.aos = aos;
   for (int t = 0; t < 4; t++) {
     B2S_CHECK_PTR(ar[t], "input re train"); B2S_CHECK_PTR(ai[t], "input im train");
     B2S_CHECK_PTR(ur[t], "u_re train"); B2S_CHECK_PTR(ui[t], "u_im train");
@@ -765,6 +817,27 @@ int b2s_svd2_complex(int64_t n, const double* const a_re[4], const double* const
                      void* stream) {
   return cplx_entry(n, a_re, a_im, u_re, u_im, v_re, v_im, smax, smin, shift, backscale_mode, flags, states,
                     (cudaStream_t)stream);
+}
+
+int b2s_svd2_real_records(int64_t n, const double* records, double* const u[4], double* const v[4],
+                          double* smax, double* smin, double* shift, int backscale_mode, int flags,
+                          void* stream) {
+  if (flags & B2S_FLAG_STATES) return fail(3, "state dumps need SoA trains (b2s_svd2_real)");
+  if (!records) return fail(5, "records is NULL");
+  if (((uintptr_t)records & 15u) != 0) return fail(6, "records must be 16-byte aligned");
+  const double* a[4] = {records, records, records, records};
+  return real_entry(n, a, u, v, smax, smin, shift, backscale_mode, flags, nullptr, (cudaStream_t)stream, 1);
+}
+
+int b2s_svd2_complex_records(int64_t n, const double* records, double* const u_re[4], double* const u_im[4],
+                             double* const v_re[4], double* const v_im[4], double* smax, double* smin,
+                             double* shift, int backscale_mode, int flags, void* stream) {
+  if (flags & B2S_FLAG_STATES) return fail(3, "state dumps need SoA trains (b2s_svd2_complex)");
+  if (!records) return fail(5, "records is NULL");
+  if (((uintptr_t)records & 15u) != 0) return fail(6, "records must be 16-byte aligned");
+  const double* a[4] = {records, records, records, records};
+  return cplx_entry(n, a, a, u_re, u_im, v_re, v_im, smax, smin, shift, backscale_mode, flags, nullptr,
+                    (cudaStream_t)stream, 1);
 }
 
 int b2s_backscale(int64_t n, const double* smax, const double* smin, const double* shift, int backscale_mode,

@@ -231,3 +231,19 @@ def test_hard_lane_queue_counts():
         c = _lib.lib.b2s_hard_lane_count(0)
         assert 0 <= c <= bound * n, (config, c)
         print("config %d: %d hard lanes of %d" % (config, c, n))
+
+
+@pytest.mark.parametrize("field,n", [("real", 300_005), ("complex", 77_777), ("real", 8), ("complex", 1 << 16)])
+def test_record_ingest_equals_trains(field, n):
+    """Direct AoSoA-8 ingest (TMA blocks of 32 records) == SoA trains."""
+    from paper_2005_07403_b200 import records as R
+    rng = np.random.default_rng(n)
+    k = 8 if field == "complex" else 4
+    v = rng.integers(0, 2 ** 64, size=(k, n), dtype=np.uint64).view(np.float64).copy()
+    v[~np.isfinite(v)] = 0.5
+    re, im = (v[0::2], v[1::2]) if field == "complex" else (v, None)
+    recs = R.trains_to_records(re, im)
+    out = R.run_records(recs, n, field).cpu()
+    ref = oracle.svd2(b2s.from_trains(re, im).re, b2s.from_trains(re, im).im)
+    for name, arr in ref.trains().items():
+        assert_bits_equal(out.trains()[name], arr, name)

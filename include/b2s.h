@@ -138,6 +138,28 @@ int b2s_synth(int config, uint64_t seed, int64_t lane0, int64_t n,
               double *const re[4], double *const im[4], void *stream);
 
 /*
+ * Batch quality metrics in double-double (lanesvd.verify.metrics,
+ * verify.py:355-477), bit-identical per lane to the reference: relative
+ * residual rho, unitarity defects delta (U) and eta (V), condition number
+ * kappa as (exponent d, double-double mantissa), evaluated in the domain the
+ * stored values live in (A when the shift is the -0.0 backscale sentinel,
+ * 2^shift A otherwise).  Device trains: a_im / u_im / v_im NULL for real
+ * batches.  Writes one partial record of 11 doubles per block into
+ * `partial` ([blocks][11]: rho hi, lo, delta hi, lo, eta hi, lo, kappa d,
+ * kappa hi, kappa lo, kappa-infinite flag, excluded-lane count), each an
+ * exact lexicographic maximum (sum for the count) over the block's lanes;
+ * the caller folds the partials the same way.  lane_rho / lane_delta /
+ * lane_eta: optional per-lane high parts (NULL to skip).
+ */
+int b2s_metrics(int64_t n, const double *const a_re[4],
+                const double *const a_im[4], const double *const u_re[4],
+                const double *const u_im[4], const double *const v_re[4],
+                const double *const v_im[4], const double *smax,
+                const double *smin, const double *shift, double *partial,
+                int blocks, double *lane_rho, double *lane_delta,
+                double *lane_eta, void *stream);
+
+/*
  * Pre-allocate the per-device hard-lane mask for launches of up to `lanes`
  * lanes.  The fast kernels evaluate every division / sqrt with inline
  * sequences whose operand ranges the scaling phase guarantees; lanes whose

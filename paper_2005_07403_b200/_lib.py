@@ -27,7 +27,7 @@ SYMBOLS = (
     "b2s_svd2_real_host", "b2s_svd2_complex_host", "b2s_backscale",
     "b2s_synth", "b2s_check_fp_env", "b2s_math_probe",
     "b2s_reserve_workspace", "b2s_hard_lane_count",
-    "b2s_svd2_real_records", "b2s_svd2_complex_records",
+    "b2s_svd2_real_records", "b2s_svd2_complex_records", "b2s_metrics",
 )
 
 _P = ctypes.c_void_p
@@ -60,6 +60,8 @@ def _load():
     L.b2s_check_fp_env.argtypes = [_int]
     L.b2s_math_probe.argtypes = [_int, _i64, _P, _P, _P, _P]
     L.b2s_reserve_workspace.argtypes = [_int, _i64]
+    L.b2s_metrics.argtypes = [_i64, _PA, _PA, _PA, _PA, _PA, _PA, _P, _P, _P,
+                              _P, _int, _P, _P, _P, _P]
     L.b2s_svd2_real_records.argtypes = [_i64, _P, _PA, _PA, _P, _P, _P, _int,
                                         _int, _P]
     L.b2s_svd2_complex_records.argtypes = [_i64, _P, _PA, _PA, _PA, _PA, _P,

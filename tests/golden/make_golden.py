@@ -199,7 +199,53 @@ def main():
         lane_record("config%d" % config, re, im, store, states=False)
     np.savez_compressed(os.path.join(HERE, "lanes.npz"), **store)
     print("wrote", len(store), "arrays")
+    write_metrics()
+
+
+def _mstr(x):
+    import mpmath
+    with mpmath.workprec(240):
+        return mpmath.nstr(x, 80)
+
+
+def write_metrics():
+    """Reference verify.metrics (double-double) for GPU-verifier parity."""
+    from lanesvd import verify
+    res = {}
+    data = np.load(os.path.join(HERE, "lanes.npz"))
+    recs = {}
+    for key in data.files:
+        rec, name = key.split("/", 1)
+        recs.setdefault(rec, {})[name] = data[key]
+    for name in ("fuzz_real", "fuzz_complex", "zeros_real", "zeros_complex",
+                 "patterned_real", "patterned_real_safe", "fuzz_real_safe",
+                 "fuzz_real_unc", "config2", "config4"):
+        rec = recs[name]
+        b = layout.from_trains(rec["in_re"], rec.get("in_im"))
+        out = layout.SvdBatchOut(n=b.n, u_re=rec["u_re"], u_im=rec.get("u_im"),
+                                 v_re=rec["v_re"], v_im=rec.get("v_im"),
+                                 smax=rec["smax"], smin=rec["smin"], shift=rec["shift"])
+        m = verify.metrics(b, out)
+        res[name] = {"kappa": _mstr(m.kappa), "rho": _mstr(m.rho), "delta": _mstr(m.delta),
+                     "eta": _mstr(m.eta), "excluded": m.rho_excluded_lanes}
+    for config in (0, 1):
+        n = synth.CONFIGS[config]["n"]
+        re, im = synth.generate(config, SEED, 0, n)
+        out = ref_run(re, im)
+        b = layout.from_trains(re, im)
+        o = layout.SvdBatchOut(n=n, u_re=out.u_re, u_im=out.u_im, v_re=out.v_re, v_im=out.v_im,
+                               smax=out.smax, smin=out.smin, shift=out.shift)
+        m = verify.metrics(b, o)
+        res["config%d_full" % config] = {"kappa": _mstr(m.kappa), "rho": _mstr(m.rho),
+                                         "delta": _mstr(m.delta), "eta": _mstr(m.eta),
+                                         "excluded": m.rho_excluded_lanes}
+        print("metrics config", config, res["config%d_full" % config], flush=True)
+    with open(os.path.join(HERE, "metrics.json"), "w") as fh:
+        json.dump(res, fh, indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
-    main()
+    if "--metrics-only" in sys.argv:
+        write_metrics()
+    else:
+        main()

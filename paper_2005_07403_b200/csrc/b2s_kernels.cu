@@ -80,7 +80,9 @@ __device__ __forceinline__ void store_states(double* const* st, int64_t i, const
 }
 
 template <int Mode>
-__device__ __forceinline__ void store_real(const RealArgs& A, int64_t i, RealOut o) {
+// i < 2^31 (one sub-launch): 32-bit lane offsets let every address be a
+// single IMAD.WIDE.U32 off the train base.
+__device__ __forceinline__ void store_real(const RealArgs& A, uint32_t i, RealOut o) {
   backscale_lane<Mode>(o.smax, o.smin, o.shift);
   #pragma unroll
   for (int t = 0; t < 4; t++) st_stream(A.u[t] + i, o.u[t]);
@@ -92,7 +94,7 @@ __device__ __forceinline__ void store_real(const RealArgs& A, int64_t i, RealOut
 }
 
 template <int Mode>
-__device__ __forceinline__ void store_cplx(const CplxArgs& A, int64_t i, CplxOut o) {
+__device__ __forceinline__ void store_cplx(const CplxArgs& A, uint32_t i, CplxOut o) {
   backscale_lane<Mode>(o.smax, o.smin, o.shift);
   #pragma unroll
   for (int t = 0; t < 4; t++) { st_stream(A.ur[t] + i, o.ur[t]); st_stream(A.ui[t] + i, o.ui[t]); }

@@ -178,18 +178,28 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   const double num = mul(mul(lo, 2.0), hi);                  // scalef(min, 1) * max
   const double den = fma_(sub(x, y), add(x, y), 1.0);         // in [0, 2]
   // num / den: num == 0 gives +0 or NaN (den == 0), both absorbed to +0.
-  // (Cheap in both variants: it flags ~0.6% of config-4 lanes, cheaper to
-  // fix than to normalise for every wide warp.)
-  double qn = quot_f(num, den, rcp_f(den));
-  const bool hn = nz_(num) && !(resid_ok(hi_(num)) && normal_q(hi_(qn)));
+  double qn;
+  bool hn = false;
+  if (Wide) {
+    qn = div_den<true, Fix>(num, make_den<Fix>(den), hn);
+  } else {
+    qn = quot_f(num, den, rcp_f(den));
+    hn = nz_(num) && !(resid_ok(hi_(num)) && normal_q(hi_(qn)));
+  }
   if (Fix) { if (hn) qn = div_fix(num, den); } else hard |= hn;
   const double tan2 = or_(rmin(rmax(qn, 0.0), kSqrtDblMax()), kNegZero());
   // tan2 in [-sqrt(DBL_MAX), -0]; the denominator is in [2, 2^512].
   const double den2 = add(1.0, sqrt_f(fma_(tan2, tan2, 1.0)));
-  const double ql = quot_f(tan2, den2, rcp_f(den2));
-  double lt = mk_(lop_or(hi_(ql), 0x80000000u), lo_(ql));   // sign of -0 / den2
-  const bool hl = nz_(tan2) && !(resid_ok(lop_and(hi_(tan2), 0x7FFFFFFFu)) &&
-                                 normal_q(lop_and(hi_(ql), 0x7FFFFFFFu)));
+  double lt;
+  bool hl = false;
+  if (Wide) {
+    lt = div_den<false, Fix>(tan2, make_den<Fix>(den2), hl);
+  } else {
+    const double ql = quot_f(tan2, den2, rcp_f(den2));
+    lt = mk_(lop_or(hi_(ql), 0x80000000u), lo_(ql));   // sign of -0 / den2
+    hl = nz_(tan2) && !(resid_ok(lop_and(hi_(tan2), 0x7FFFFFFFu)) &&
+                        normal_q(lop_and(hi_(ql), 0x7FFFFFFFu)));
+  }
   if (Fix) { if (hl) lt = div_fix(tan2, den2); } else hard |= hl;
   const double ls2 = fma_(lt, lt, 1.0);
   const double rt = fma_(y, lt, -x);

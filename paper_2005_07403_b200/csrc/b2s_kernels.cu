@@ -452,7 +452,51 @@ __global__ void __launch_bounds__(kBlock, 4) k_ring_probe(const RealArgs A, int 
     A.u[1][i] = a[1];
     A.u[2][i] = a[2];
     A.u[3][i] = a[3];
+    if (A.v[0]) {                          // traffic probe: the SVD kernel's 11 output trains
+      #pragma unroll
+      for (int t = 0; t < 4; t++) st_stream(A.v[t] + i, a[t]);
+      st_stream(A.smax + i, a[0]);
+      st_stream(A.smin + i, a[1]);
+      st_stream(A.shift + i, a[2]);
+    }
   }
+}
+
+// Diagnostic: the same traffic shape with the output side staged through
+// shared memory and written by bulk (TMA) stores, 11 x 2 KiB per 256-lane
+// tile, double-buffered, one CTA barrier per tile.
+__global__ void __launch_bounds__(kBlock, 2) k_traffic_bulk(const RealArgs A) {
+  extern __shared__ __align__(128) char smem[];
+  const double* src[4] = {A.a[0], A.a[1], A.a[2], A.a[3]};
+  double* dst[11] = {A.u[0], A.u[1], A.u[2], A.u[3], A.v[0], A.v[1], A.v[2], A.v[3], A.smax, A.smin, A.shift};
+  const int tid = threadIdx.x;
+  const int64_t tiles = A.n / kBlock;
+  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  TmaRing<4> R;
+  R.init(smem, src, mine);
+  double* stagebuf = reinterpret_cast<double*>(smem + (TmaRing<4>::kSmem + 127) / 128 * 128);
+  for (int64_t k = 0; k < mine; k++) {
+    const int s = (int)(k % kStages);
+    R.wait_full(k);
+    double a[4];
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = R.stage(s, t)[tid];
+    consumed(a);
+    R.release(k);
+    double* ob = stagebuf + (size_t)(k & 1) * 11 * kBlock;
+    #pragma unroll
+    for (int t = 0; t < 11; t++) ob[t * kBlock + tid] = a[t & 3];
+    tma::fence_proxy_async();
+    if (tid == 0) tma::bulk_wait_read<0>();
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t base = R.tile(k) * kBlock;
+      #pragma unroll
+      for (int t = 0; t < 11; t++) tma::bulk_store(dst[t] + base, ob + t * kBlock, kBlock * 8);
+      tma::bulk_commit();
+    }
+  }
+  if (tid == 0) tma::bulk_wait<0>();
 }
 
 // Exact fix-up of the marked hard lanes.  Each warp takes 32 mask words
@@ -906,10 +950,25 @@ long long b2s_hard_lane_count(int device) {
   return out;
 }
 
-int b2s_ring_probe(int64_t n, const double* const a[4], double* const out[4], int spin, void* stream) {
+int b2s_traffic_bulk(int64_t n, const double* const a[4], double* const out[11], void* stream) {
   RealArgs A{};
   A.n = n;
-  for (int t = 0; t < 4; t++) { A.a[t] = a[t]; A.u[t] = out[t]; }
+  for (int t = 0; t < 4; t++) { A.a[t] = a[t]; A.u[t] = out[t]; A.v[t] = out[4 + t]; }
+  A.smax = out[8]; A.smin = out[9]; A.shift = out[10];
+  const size_t sm = (TmaRing<4>::kSmem + 127) / 128 * 128 + 2 * 11 * kBlock * sizeof(double);
+  B2S_CUDA(cudaFuncSetAttribute(k_traffic_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_traffic_bulk<<<tma_grid(k_traffic_bulk, sm, n), kBlock, sm, (cudaStream_t)stream>>>(A);
+  B2S_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// Diagnostic (tests / tools): spin == 1000000 selects the 11-output traffic
+// probe (out[0..10]), otherwise the 4-train ring copy with busy work.
+int b2s_ring_probe(int64_t n, const double* const a[4], double* const out[11], int spin, void* stream) {
+  RealArgs A{};
+  A.n = n;
+  for (int t = 0; t < 4; t++) { A.a[t] = a[t]; A.u[t] = out[t]; A.v[t] = spin == 1000000 ? out[4 + t] : nullptr; }
+  if (spin == 1000000) { A.smax = out[8]; A.smin = out[9]; A.shift = out[10]; spin = 0; }
   const size_t sm = TmaRing<4>::kSmem;
   B2S_CUDA(cudaFuncSetAttribute(k_ring_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_ring_probe<<<tma_grid(k_ring_probe, sm, n), kBlock, sm, (cudaStream_t)stream>>>(A, spin);

@@ -144,11 +144,13 @@ int b2s_synth(int config, uint64_t seed, int64_t lane0, int64_t n,
  * kappa as (exponent d, double-double mantissa), evaluated in the domain the
  * stored values live in (A when the shift is the -0.0 backscale sentinel,
  * 2^shift A otherwise).  Device trains: a_im / u_im / v_im NULL for real
- * batches.  Writes one partial record of 11 doubles per block into
- * `partial` ([blocks][11]: rho hi, lo, delta hi, lo, eta hi, lo, kappa d,
- * kappa hi, kappa lo, kappa-infinite flag, excluded-lane count), each an
- * exact lexicographic maximum (sum for the count) over the block's lanes;
- * the caller folds the partials the same way.  lane_rho / lane_delta /
+ * batches.  Writes one partial record of 15 doubles per block into
+ * `partial` ([blocks][15]: rho hi, lo, delta hi, lo, eta hi, lo, kappa d,
+ * kappa hi, kappa lo, kappa-infinite flag, excluded-lane count, and the
+ * spectral-norm unitarity defects |U*U - I|_2 hi, lo, |V*V - I|_2 hi, lo --
+ * an extension beyond the reference), each an exact lexicographic maximum
+ * (sum for the count) over the block's lanes; the caller folds the partials
+ * the same way.  lane_rho / lane_delta /
  * lane_eta: optional per-lane high parts (NULL to skip).
  */
 int b2s_metrics(int64_t n, const double *const a_re[4],

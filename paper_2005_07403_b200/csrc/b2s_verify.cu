@@ -145,14 +145,30 @@ __device__ __forceinline__ DD gram_deviation(CD c11, CD c21, CD c12, CD c22) {
   return sqrt(s);
 }
 
+// Spectral-norm companion of gram_deviation (an extension for the
+// north-star tolerance report): |G|_2 of the Hermitian
+// G = C*C - I is |tr G| / 2 + sqrt(((g11 - g22) / 2)^2 + |g12|^2).
+__device__ __forceinline__ DD gram_deviation2(CD c11, CD c21, CD c12, CD c22) {
+  const DD one = from(1.0);
+  const DD g11 = sub(add(abs2(c11), abs2(c21)), one);
+  const DD g22 = sub(add(abs2(c12), abs2(c22)), one);
+  const CD g12 = cadd(cmul(conj(c11), c12), cmul(conj(c21), c22));
+  DD half_tr = scalb(add(g11, g22), -1.0);
+  if (half_tr.hi < 0.0) half_tr = neg(half_tr);
+  const DD half_df = scalb(sub(g11, g22), -1.0);
+  return add(half_tr, sqrt(add(mul(half_df, half_df), abs2(g12))));
+}
+
 }  // namespace dd
 
 // Per-block partial: rho, delta, eta (hi, lo), kappa (d, qhi, qlo), kappa
-// infinite flag, excluded-lane count.
-constexpr int kPartial = 11;
+// infinite flag, excluded-lane count, then the spectral-norm delta2, eta2
+// (hi, lo).
+constexpr int kPartial = 15;
 
 struct Acc {
   double rho_hi, rho_lo, del_hi, del_lo, eta_hi, eta_lo, kd, kq_hi, kq_lo, kinf, bad;
+  double d2_hi, d2_lo, e2_hi, e2_lo;
 };
 
 // Lexicographic maximum helpers (NaN in hi propagates, like numpy.max).
@@ -177,11 +193,13 @@ __device__ __forceinline__ void merge(Acc& a, const Acc& b) {
   max_kappa(a, b.kd, b.kq_hi, b.kq_lo);
   a.kinf = fmax(a.kinf, b.kinf);
   a.bad += b.bad;
+  max_dd(a.d2_hi, a.d2_lo, b.d2_hi, b.d2_lo);
+  max_dd(a.e2_hi, a.e2_lo, b.e2_hi, b.e2_lo);
 }
 
 __device__ __forceinline__ Acc acc_identity() {
   const double ninf = -__longlong_as_double(0x7FF0000000000000ll);
-  return {ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, 0.0, 0.0};
+  return {ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, 0.0, 0.0, ninf, ninf, ninf, ninf};
 }
 
 struct MetricArgs {
@@ -236,6 +254,10 @@ __device__ Acc lane_metrics(const MetricArgs& M, int64_t i) {
   r.del_hi = delta.hi; r.del_lo = delta.lo;
   r.eta_hi = eta.hi; r.eta_lo = eta.lo;
   r.bad = bad ? 1.0 : 0.0;
+  const DD d2 = gram_deviation2(u[0], u[1], u[2], u[3]);
+  const DD e2 = gram_deviation2(v[0], v[1], v[2], v[3]);
+  r.d2_hi = d2.hi; r.d2_lo = d2.lo;
+  r.e2_hi = e2.hi; r.e2_lo = e2.lo;
   if (bad || smin == 0.0) {
     r.kinf = 1.0;
   } else {

@@ -21,7 +21,7 @@ from .layout import is_device_array
 
 __all__ = ["Metrics", "metrics", "lane_metrics", "fold_partials"]
 
-_NPART = 11
+_NPART = 15
 
 
 @dataclass
@@ -92,7 +92,8 @@ def fold_partials(p):
     sel &= p[:, 7] == qhi
     qlo = np.max(p[sel, 8])
     return {"rho": rho, "delta": delta, "eta": eta, "kappa": (dmax, qhi, qlo),
-            "kappa_inf": bool(np.max(p[:, 9]) > 0), "excluded": int(np.sum(p[:, 10]))}
+            "kappa_inf": bool(np.max(p[:, 9]) > 0), "excluded": int(np.sum(p[:, 10])),
+            "delta2": dd_max(p[:, 11], p[:, 12]), "eta2": dd_max(p[:, 13], p[:, 14])}
 
 
 def metrics(batch, out):

@@ -247,3 +247,47 @@ def test_record_ingest_equals_trains(field, n):
     ref = oracle.svd2(b2s.from_trains(re, im).re, b2s.from_trains(re, im).im)
     for name, arr in ref.trains().items():
         assert_bits_equal(out.trains()[name], arr, name)
+
+
+def test_misaligned_trains_take_ldg_path():
+    """Trains only 8-byte aligned (odd lane offset) cannot feed the TMA ring;
+    the register-prefetch kernels run instead, with identical results."""
+    n = 50_001
+    re, im = synth.generate_device(1, 3, 0, n + 1, device=DEV)
+    re_v = [re[t][1:] for t in range(4)]          # 8-byte aligned views
+    im_v = [im[t][1:] for t in range(4)]
+    assert re_v[0].data_ptr() % 16 == 8
+    out = b2s.SvdBatchOut.empty(n, True, device=DEV)
+    outd = {"u_re": list(out.u_re), "u_im": list(out.u_im), "v_re": list(out.v_re),
+            "v_im": list(out.v_im), "smax": out.smax, "smin": out.smin, "shift": out.shift}
+    from paper_2005_07403_b200.svd2 import launch_device
+    launch_device(n, re_v, im_v, outd, 0)
+    torch.cuda.synchronize()
+    ref = oracle.svd2(re[:, 1:].cpu().numpy(), im[:, 1:].cpu().numpy())
+    host = out.cpu()
+    for name, arr in ref.trains().items():
+        assert_bits_equal(host.trains()[name][..., :n], arr, name)
+
+
+def test_nonfinite_inputs_do_not_hang():
+    """Non-finite entries are rejected at ingest (pack / from_trains, as in
+    layout.py:133-186); fed raw to the kernels they must still terminate."""
+    re = torch.tensor([[np.nan, np.inf, -np.inf, 1.0, 0.0, 1.0, 5e-324, 1e308]] * 4,
+                      dtype=torch.float64, device=DEV)
+    out, _ = b2s.run_batch(Batch2x2(n=8, re=re), b2s.RunConfig())
+    torch.cuda.synchronize()
+    assert out.smax.shape == (8,)
+    with pytest.raises(ValueError):
+        b2s.pack(np.full((1, 2, 2), np.nan))
+
+
+def test_sub_launch_boundaries_small_chunk_host_path():
+    """Host pipeline chunk edges at arbitrary positions (ragged tails)."""
+    n = 10_007
+    re, _ = synth.generate(2, 8, 0, n)
+    b = from_trains(re)
+    ref = oracle.svd2(b.re)
+    for chunk in (256, 1000, 4096):
+        out, _ = b2s.run_batch(b, b2s.RunConfig(chunk=chunk))
+        for k, arr in ref.trains().items():
+            assert_bits_equal(out.trains()[k], arr, "%s chunk=%d" % (k, chunk))

@@ -195,6 +195,9 @@ int b2s_check_fp_env(int device);
  *     and normal b, subnormal quotients included)
  *   7 / 8 cos / sin of phase_from_parts(a, b, hypot(a, b)) (lanes.py:248-259)
  *   9 a / b for 0 <= a <= b < 2^1023 (the streaming kernels' checked site)
+ *  10 / 11 op 6 as the streaming kernels evaluate it (normal operands
+ *     only; subnormal quotients rounded by the warp-uniform FP64 sequence /
+ *     by the integer re-rounding call)
  * Checked ops write the NaN pattern 0x7FF4DEADBEEF0000 where the fast path
  * declines (the kernels recompute such lanes exactly).  b may be NULL for
  * ops 1-3.

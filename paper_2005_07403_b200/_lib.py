@@ -13,7 +13,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libb2s.so")
+# B2S_LIBRARY selects another build of the same ABI (A/B kernel variants
+# from `build.py --out PATH -DNAME=VALUE`); the default is the in-tree build.
+LIB_PATH = os.environ.get("B2S_LIBRARY") or os.path.join(_HERE, "_native", "libb2s.so")
 
 BACKSCALE = {"none": 0, "safe": 1, "unconditional": 2}
 FLAG_SINE_FORM = 1

@@ -31,21 +31,27 @@ def _stale():
     return any(os.path.getmtime(os.path.join(HERE, p)) > t for p in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile the library (to `out` with extra -D `defines` for A/B
+    variants; those are always rebuilt)."""
+    if out is None and not force and not _stale():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    target = out or OUT
+    os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists("/usr/local/cuda/bin/nvcc") and nvcc == "nvcc":
         pass
     elif nvcc == "nvcc" and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-        ["-o", OUT + ".tmp"] + [os.path.join(HERE, s) for s in SOURCES]
+    cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + list(defines) + \
+        ["-o", target + ".tmp"] + [os.path.join(HERE, s) for s in SOURCES]
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else None
+    print(build(force="--force" in argv, verbose="-v" in argv, out=out,
+                defines=[a for a in argv if a.startswith("-D")]))

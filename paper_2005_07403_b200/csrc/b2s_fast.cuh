@@ -45,7 +45,7 @@ __device__ __forceinline__ double div_pos_f(double a, double b, bool& hard) {
   const bool z = !nz_(a);
   const double d = z ? 1.0 : b;
   double q = quot_f(a, d, rcp_f(d));
-  const bool h = !z && !(resid_ok(hi_(a)) && normal_q(hi_(q)));
+  const bool h = !z & !(resid_ok(hi_(a)) & normal_q(hi_(q)));
   if (Fix) { if (h) q = div_fix(a, b); } else hard |= h;
   return q;
 }
@@ -59,7 +59,7 @@ __device__ __forceinline__ double div_pos_big_f(double a, double b, bool& hard) 
   const double a2 = mul(a, sc);
   const double d = z ? 1.0 : mul(b, sc);
   double q = quot_f(a2, d, rcp_f(d));
-  const bool h = !z && !(resid_ok(hi_(a2)) && normal_q(hi_(q)));
+  const bool h = !z & !(resid_ok(hi_(a2)) & normal_q(hi_(q)));
   if (Fix) { if (h) q = div_fix(a, b); } else hard |= h;
   return q;
 }
@@ -78,7 +78,7 @@ __device__ __forceinline__ double hypot_f(double m1, double m2, bool& hard) {
   maxmin(m1, m2, big, small);
   bool h = false;
   double q = div_pos_f<false>(small, big, h);   // = small / max(big, TRUE_MIN)
-  h = h && !hypot_q_irrelevant(q);
+  h = h & !hypot_q_irrelevant(q);
   if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
   return mul(big, sqrt_f(fma_(q, q, 1.0)));
 }
@@ -91,7 +91,7 @@ __device__ __forceinline__ double hypot_big_f(double m1, double m2, bool& hard) 
   maxmin(m1, m2, big, small);
   bool h = false;
   double q = div_pos_big_f<false>(small, big, h);
-  h = h && !hypot_q_irrelevant(q);
+  h = h & !hypot_q_irrelevant(q);
   if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
   return mul(big, sqrt_f(fma_(q, q, 1.0)));
 }
@@ -127,14 +127,20 @@ __device__ __forceinline__ void phase_f(double re, double im, double mag, double
   // A zero part gives an exactly zero quotient (0 / mag); it is selected
   // directly so that a garbage reciprocal (subnormal mag, flagged through
   // the other part) can never leak through it.
+  // The streaming kernel (Fix = false) skips those selects: a garbage
+  // reciprocal only arises for a subnormal mag, whose nonzero part is itself
+  // subnormal and flags the lane below; with a usable reciprocal a zero part
+  // already gives an exact zero quotient (signed through the OR).
   const double a1 = mul(fabs_(re), sc);
   const double q1 = quot_f(a1, d, r);
-  c = or_(mz ? 1.0 : (nz_(re) ? rmin(q1, 1.0) : 0.0), sgn_(re));
+  const double cm = rmin(q1, 1.0);
+  c = or_(mz ? 1.0 : (Fix ? (nz_(re) ? cm : 0.0) : cm), sgn_(re));
   const double a2 = mul(im, sc);
   const double q2 = quot_f(a2, d, r);
-  s = nz_(im) ? mk_(lop_or(lop_and(hi_(q2), 0x7FFFFFFFu), lop_and(hi_(im), 0x80000000u)), lo_(q2)) : im;
-  const bool hc = nz_(a1) && !(resid_ok(hi_(a1)) && normal_q(hi_(q1)));
-  const bool hs = nz_(im) && !(resid_ok(lop_and(hi_(a2), 0x7FFFFFFFu)) && normal_q(lop_and(hi_(q2), 0x7FFFFFFFu)));
+  const double sq = mk_(lop_or(lop_and(hi_(q2), 0x7FFFFFFFu), lop_and(hi_(im), 0x80000000u)), lo_(q2));
+  s = Fix ? (nz_(im) ? sq : im) : sq;
+  const bool hc = nz_(a1) & !(resid_ok(hi_(a1)) & normal_q(hi_(q1)));
+  const bool hs = nz_(im) & !(resid_ok(lop_and(hi_(a2), 0x7FFFFFFFu)) & normal_q(lop_and(hi_(q2), 0x7FFFFFFFu)));
   if (Fix) {
     if (hc) c = or_(rmin(div_fix(fabs_(re), mag), 1.0), sgn_(re));
     if (hs) s = div_fix(im, rmax(mag, kTrueMin()));
@@ -163,8 +169,8 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
     const double a12 = mul(r12, 0.25), a22 = mul(r22, 0.25);
     qx = quot_f(a12, b, r);
     qy = quot_f(a22, b, r);
-    hx = nz_(r12) && !(resid_ok(hi_(a12)) && normal_q(hi_(qx)));
-    hy = nz_(r22) && !(resid_ok(hi_(a22)) && normal_q(hi_(qy)));
+    hx = nz_(r12) & !(resid_ok(hi_(a12)) & normal_q(hi_(qx)));
+    hy = nz_(r22) & !(resid_ok(hi_(a22)) & normal_q(hi_(qy)));
   }
   if (Fix) {
     if (hx) qx = div_fix(r12, r11);
@@ -184,7 +190,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
     qn = div_den<true, Fix>(num, make_den<Fix>(den), hn);
   } else {
     qn = quot_f(num, den, rcp_f(den));
-    hn = nz_(num) && !(resid_ok(hi_(num)) && normal_q(hi_(qn)));
+    hn = nz_(num) & !(resid_ok(hi_(num)) & normal_q(hi_(qn)));
   }
   if (Fix) { if (hn) qn = div_fix(num, den); } else hard |= hn;
   const double tan2 = or_(rmin(rmax(qn, 0.0), kSqrtDblMax()), kNegZero());
@@ -197,7 +203,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   } else {
     const double ql = quot_f(tan2, den2, rcp_f(den2));
     lt = mk_(lop_or(hi_(ql), 0x80000000u), lo_(ql));   // sign of -0 / den2
-    hl = nz_(tan2) && !(resid_ok(lop_and(hi_(tan2), 0x7FFFFFFFu)) &&
+    hl = nz_(tan2) & !(resid_ok(lop_and(hi_(tan2), 0x7FFFFFFFu)) &
                         normal_q(lop_and(hi_(ql), 0x7FFFFFFFu)));
   }
   if (Fix) { if (hl) lt = div_fix(tan2, den2); } else hard |= hl;

@@ -143,6 +143,46 @@ def test_normalised_division_full_range(gen):
     assert (bits(probe(6, a[:4], z)) == HARD).all()
 
 
+@pytest.mark.parametrize("op", [10, 11])
+def test_normalised_division_streaming_variant(gen, op):
+    """div_den as the streaming kernels run it: selects instead of per-lane
+    branches, subnormal quotients rounded by the warp-uniform FP64 sequence
+    (op 10) or the integer re-rounding call (op 11).  Exact for every normal /
+    zero numerator over a normal denominator; declines subnormal operands."""
+    sgn = lambda: torch.where(torch.rand(N, device=DEV, generator=gen) < 0.5, -1.0, 1.0).to(torch.float64)
+    for (la, ha), (lb, hb) in (((-1022, 1023), (-1022, 1023)), ((-1022, -900), (900, 1023)),
+                               ((-1022, -1000), (0, 80)), ((-200, 0), (850, 1023)),
+                               ((1000, 1023), (-1022, -1000)), ((-60, 60), (-60, 60))):
+        a = rand_mag(N, la, ha, gen) * sgn()
+        b = rand_mag(N, lb, hb, gen) * sgn()
+        a[:1000] = 0.0
+        a[1000:2000] = -0.0
+        q = probe(op, a, b)
+        assert not (bits(q) == HARD).any()
+        assert_same(q, a / b, "streaming div_den [%d,%d]/[%d,%d]" % (la, ha, lb, hb))
+    # exact midpoints of the subnormal grid and their neighbours: a / d =
+    # (2k+1) 2^-s exactly, s spanning every subnormal rounding position
+    D = 1.0 + torch.randint(0, 1024, (N,), device=DEV, generator=gen).to(torch.float64) / 1024.0
+    k = torch.randint(0, 1 << 20, (N,), device=DEV, generator=gen).to(torch.float64)
+    s = torch.randint(1023, 1080, (N,), device=DEV, generator=gen)
+    d = D * 2.0 ** 1000
+    for nudge in (0, 1, -1):
+        a = D * (2 * k + 1)
+        a = torch.ldexp(a, (1000 - s).to(torch.float64))
+        a = a.view(torch.int64).add(nudge).view(torch.float64)    # one ulp off the midpoint
+        a = a * sgn()
+        ok = a != 0
+        q = probe(op, a[ok], d[ok])
+        assert_same(q, a[ok] / d[ok], "streaming div_den ties nudge=%d" % nudge)
+    # subnormal operands are declined, never wrong
+    a = rand_mag(N, -1074, -1023, gen)
+    b = rand_mag(N, 0, 10, gen)
+    q = probe(op, a, b)
+    assert (bits(q) == HARD).all()
+    q = probe(op, b, a)
+    assert (bits(q) == HARD).all()
+
+
 def test_hypot_never_wrong(gen):
     import oracle
     for lo, hi in ((1015, 1022), (-1074, 1022), (-30, 30)):

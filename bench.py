@@ -119,13 +119,22 @@ class Clocks:
 
 
 def dist_init():
+    """One process per GPU (torchrun env).  B2S_DIST_BACKEND=gloo with more
+    ranks than GPUs (ranks share devices round-robin) exercises the
+    multi-rank path -- sharding, barriers, max over ranks, rank-0 output --
+    on a single-GPU box; its timings are not scaling numbers."""
     from paper_2005_07403_b200.dist import world_info
     world, rank, local = world_info()
     if world > 1:
         import torch
         import torch.distributed as dist
+        backend = os.environ.get("B2S_DIST_BACKEND", "nccl")
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 

@@ -217,7 +217,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
 // norm is < 2^1022.5 and the pivot magnitude m11 (>= n1 / sqrt 2) lies in
 // [2^1020.5, 2^1022) unless the matrix is zero.
 // ---------------------------------------------------------------------------
-template <bool Sine, bool Fix>
+template <bool Sine, bool Fix, bool Wide = false>
 __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   bool hard = false;
   double e[4] = {a[0], a[1], a[2], a[3]};
@@ -239,14 +239,20 @@ __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   U.ph1 = sgn_(e[0]);
   U.ph2 = sgn_(e[1]);
   const double f12 = xor_(e[2], U.ph1), f22 = xor_(e[3], U.ph2);
-  U.mt = div_pos_f<Fix>(m21, m11, hard);            // relaxed_max(., 0) is the identity here
+  if (Wide) {
+    bool h = false;
+    U.mt = div_den<false, Fix>(m21, make_den<Fix>(m11), h);   // relaxed_max(., 0) is the identity here
+    if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
+  } else {
+    U.mt = div_pos_f<Fix>(m21, m11, hard);            // relaxed_max(., 0) is the identity here
+  }
   U.cg = invsqrt_f(fma_(U.mt, U.mt, 1.0));
   const double g12 = mul(U.cg, fma_(U.mt, f22, f12));
   const double g22 = mul(U.cg, fnma_(U.mt, f12, f22));
   U.dt = sgn_(g12);
   const double w = xor_(g22, U.dt);
   U.dh = sgn_(w);
-  const Tri T = triangle_f<Fix>(r11, fabs_(g12), fabs_(w), hard);
+  const Tri T = triangle_f<Fix, Wide>(r11, fabs_(g12), fabs_(w), hard);
   assemble_real<Sine>(U, T, o);
   o.shift = shift;
   return hard;
@@ -269,6 +275,21 @@ __device__ __forceinline__ bool wide_lane(const double (&p)[N]) {
     emin = min(emin, nz_(p[i]) ? e : 0x7FF);
   }
   return emax - emin > kWideSpread;
+}
+
+// Real lanes the fast pipeline may decline: components spanning more than
+// kWideSpread binades (tiny quotients), a subnormal component, or a
+// component within 2 binades of DBL_MAX (negative scale shift).
+template <int N>
+__device__ __forceinline__ bool wide_or_sub(const double (&p)[N]) {
+  int emax = 0, emin = 0x7FF;
+  #pragma unroll
+  for (int i = 0; i < N; i++) {
+    const int e = (int)((hi_(p[i]) >> 20) & 0x7FFu);
+    emax = max(emax, e);
+    emin = min(emin, nz_(p[i]) ? e : 0x7FF);
+  }
+  return (emax - emin > kWideSpread) | (emin == 0) | (emax >= 2045);
 }
 
 // ---------------------------------------------------------------------------

@@ -243,6 +243,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // CTA 0 with ordinary loads.
 // ---------------------------------------------------------------------------
 constexpr int kStages = 4;
+#ifndef B2S_REAL_WIDE
+#define B2S_REAL_WIDE 2
+#endif
 constexpr int kWarps = kBlock / 32;
 
 // Force the loaded values into registers (scoreboard wait) before what
@@ -353,7 +356,21 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
     R.release(k);
     const int64_t i = R.tile(k) * kBlock + tid;
     RealOut o;
-    const bool hard = svd2_real_f<Sine, false>(a, o);
+    bool hard;
+#if B2S_REAL_WIDE
+    // A warp holding a full-range lane (BASELINE config 2) runs the
+    // per-site-repairing pipeline in place, with the exponent-normalised
+    // divisions at the rotation and triangle sites (B2S_REAL_WIDE 2; 1 =
+    // repairs only): exact for every lane, so nothing is left for the fix-up
+    // kernel.  Warp-uniform choice.  Config 2, 2^26 lanes: 4.85 ms with 58 %
+    // of lanes fixed up afterwards -> 3.97 ms (mode 1) -> 2.83 ms (mode 2);
+    // config 3 unchanged.
+    if (__any_sync(0xFFFFFFFFu, wide_or_sub<4>(a))) {
+      svd2_real_f<Sine, true, B2S_REAL_WIDE == 2>(a, o);
+      hard = false;
+    } else
+#endif
+    hard = svd2_real_f<Sine, false>(a, o);
     store_real<Mode>(A, i, o);
     nh += mark_hard(A.q, hard, i);
   }

@@ -40,6 +40,15 @@ __device__ __forceinline__ void maxmin(double a, double b, double& big, double& 
 // a / b for 0 <= a <= b (up to rounding), b < 2^1022; an exact +0 for a == 0
 // (the reference gives 0/b = +0, or NaN for b == 0, which every caller
 // absorbs into +0 through relaxed_max / the hypot identity).
+// Subnormal operands at the exponent-normalised sites of the streaming
+// kernels: normalised exactly on a cold per-lane branch (1) or declined to
+// the fix-up kernel (0, the default: config 4 measured 3.99 ms per 2^26
+// lanes with 0.3 % of lanes fixed up, 4.70 ms with mode 1 and none).
+#ifndef B2S_WIDE_SUB
+#define B2S_WIDE_SUB 0
+#endif
+constexpr bool kWideSub = B2S_WIDE_SUB != 0;
+
 template <bool Fix>
 __device__ __forceinline__ double div_pos_f(double a, double b, bool& hard) {
   const bool z = !nz_(a);
@@ -104,10 +113,10 @@ __device__ __forceinline__ double hypot_big_f(double m1, double m2, bool& hard) 
 template <bool Fix>
 __device__ __forceinline__ void phase_w(double re, double im, double mag, double& c, double& s, bool& hard) {
   const bool mz = !nz_(mag);
-  const Den D = make_den<Fix>(mag);
+  const Den D = make_den<Fix || kWideSub>(mag);
   bool hc = false, hs = false;
-  const double q1 = div_den<false, Fix>(fabs_(re), D, hc);
-  const double q2 = div_den<false, Fix>(im, D, hs);
+  const double q1 = div_den<false, Fix || kWideSub, !Fix>(fabs_(re), D, hc);
+  const double q2 = div_den<false, Fix || kWideSub, !Fix>(im, D, hs);
   c = or_(mz ? 1.0 : rmin(q1, 1.0), sgn_(re));
   s = q2;
   if (Fix) {
@@ -158,9 +167,9 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   if (Wide) {
     // exponent-normalised, exact for tiny ratios too (r11 = 0 only with
     // r12 = r22 = 0, giving +0 like the reference's absorbed 0/0)
-    const Den D = make_den<Fix>(r11);
-    qx = div_den<false, Fix>(r12, D, hx);
-    qy = div_den<false, Fix>(r22, D, hy);
+    const Den D = make_den<Fix || kWideSub>(r11);
+    qx = div_den<false, Fix || kWideSub, !Fix>(r12, D, hx);
+    qy = div_den<false, Fix || kWideSub, !Fix>(r22, D, hy);
   } else {
     // one shared reciprocal of r11 / 4 (r11 = 0 gives NaN quotients,
     // absorbed to +0 exactly as the reference's 0/0 is)
@@ -187,7 +196,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   double qn;
   bool hn = false;
   if (Wide) {
-    qn = div_den<true, Fix>(num, make_den<Fix>(den), hn);
+    qn = div_den<true, Fix || kWideSub, !Fix>(num, make_den<Fix || kWideSub>(den), hn);
   } else {
     qn = quot_f(num, den, rcp_f(den));
     hn = nz_(num) & !(resid_ok(hi_(num)) & normal_q(hi_(qn)));
@@ -199,7 +208,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   double lt;
   bool hl = false;
   if (Wide) {
-    lt = div_den<false, Fix>(tan2, make_den<Fix>(den2), hl);
+    lt = div_den<false, Fix || kWideSub, !Fix>(tan2, make_den<Fix || kWideSub>(den2), hl);
   } else {
     const double ql = quot_f(tan2, den2, rcp_f(den2));
     lt = mk_(lop_or(hi_(ql), 0x80000000u), lo_(ql));   // sign of -0 / den2
@@ -241,7 +250,7 @@ __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   const double f12 = xor_(e[2], U.ph1), f22 = xor_(e[3], U.ph2);
   if (Wide) {
     bool h = false;
-    U.mt = div_den<false, Fix>(m21, make_den<Fix>(m11), h);   // relaxed_max(., 0) is the identity here
+    U.mt = div_den<false, Fix || kWideSub, !Fix>(m21, make_den<Fix || kWideSub>(m11), h);   // relaxed_max(., 0) is the identity here
     if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
   } else {
     U.mt = div_pos_f<Fix>(m21, m11, hard);            // relaxed_max(., 0) is the identity here
@@ -335,7 +344,7 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
   cmul(U.c2, neg_(U.s2), er[3], ei[3], f22r, f22i);
   if (Wide) {
     bool h = false;
-    U.mt = div_den<false, Fix>(m21, make_den<Fix>(m11), h);   // m21 >= 0: relaxed_max is the identity
+    U.mt = div_den<false, Fix || kWideSub, !Fix>(m21, make_den<Fix || kWideSub>(m11), h);   // m21 >= 0: relaxed_max is the identity
     if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
   } else {
     U.mt = div_pos_big_f<Fix>(m21, m11, hard);

@@ -595,8 +595,8 @@ __global__ void __launch_bounds__(kBlock) k_math_probe(int op, int64_t n, const 
       case 5: r = scale_up(x, (int)y); break;
       case 6: r = div_den<true>(x, make_den(y), hard); break;
       case 9: r = div_pos_big_f<false>(x, y, hard); break;
-      case 10: r = div_den<true, false, 0>(x, make_den<false>(y), hard); break;
-      case 11: r = div_den<true, false, 1>(x, make_den<false>(y), hard); break;
+      case 10: r = div_den<true, false, true, 0>(x, make_den<false>(y), hard); break;
+      case 11: r = div_den<true, false, true, 1>(x, make_den<false>(y), hard); break;
       default: { double c, s; phase_f<false>(x, y, hypot_x(x, y), c, s, hard); r = (op == 7) ? c : s; } break;
     }
     o[i] = hard ? hard_marker() : r;

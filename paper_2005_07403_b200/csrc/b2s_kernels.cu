@@ -389,7 +389,10 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
 }
 
 template <int Mode, bool Sine, bool AoS>
-__global__ void __launch_bounds__(kBlock, 3) k_svd2_cplx_tma(const CplxArgs A) {
+#ifndef B2S_CPLX_MINB
+#define B2S_CPLX_MINB 3
+#endif
+__global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const CplxArgs A) {
   extern __shared__ __align__(128) char smem[];
   const double* src[8];
   #pragma unroll

@@ -37,9 +37,6 @@ __device__ __forceinline__ void maxmin(double a, double b, double& big, double& 
   small = p ? b : a;
 }
 
-// a / b for 0 <= a <= b (up to rounding), b < 2^1022; an exact +0 for a == 0
-// (the reference gives 0/b = +0, or NaN for b == 0, which every caller
-// absorbs into +0 through relaxed_max / the hypot identity).
 // Subnormal operands at the exponent-normalised sites of the streaming
 // kernels: normalised exactly on a cold per-lane branch (1) or declined to
 // the fix-up kernel (0, the default: config 4 measured 3.99 ms per 2^26
@@ -49,8 +46,26 @@ __device__ __forceinline__ void maxmin(double a, double b, double& big, double& 
 #endif
 constexpr bool kWideSub = B2S_WIDE_SUB != 0;
 
-template <bool Fix>
+// Bnd (bounded) sites.  The streaming kernels run the fast variant only on
+// warps whose every lane has its nonzero input components within
+// kWideSpread binades of each other, all normal, with a nonnegative scale
+// shift (the real kernel's `wide_or_sub` / the complex kernel's `wide_lane`
+// dispatch).  After scaling, every nonzero component then lies in
+// [2^121, 2^1022): entry moduli, column norms, the pivot modulus and the
+// cos / sin quotients of the entry phases are all >= 2^-902 and the
+// numerators >= 2^119, so those sites can never leave the range of the
+// inline sequences and carry no checks at all.  (Sites fed by rotated,
+// possibly cancelled intermediates -- r12, r22, their phases, the triangle
+// -- keep theirs.)  A zero denominator comes with a zero numerator; its
+// hi word is lifted to the smallest normal so the quotient is an exact +0.
+__device__ __forceinline__ double lift_zero(double b) { return mk_(max(hi_(b), 0x00100000u), lo_(b)); }
+
+// a / b for 0 <= a <= b (up to rounding), b < 2^1022; an exact +0 for a == 0
+// (the reference gives 0/b = +0, or NaN for b == 0, which every caller
+// absorbs into +0 through relaxed_max / the hypot identity).
+template <bool Fix, bool Bnd = false>
 __device__ __forceinline__ double div_pos_f(double a, double b, bool& hard) {
+  if (Bnd) return quot_f(a, lift_zero(b), rcp_f(lift_zero(b)));
   const bool z = !nz_(a);
   const double d = z ? 1.0 : b;
   double q = quot_f(a, d, rcp_f(d));
@@ -61,11 +76,15 @@ __device__ __forceinline__ double div_pos_f(double a, double b, bool& hard) {
 
 // Same for b < 2^1023: denominators >= 2^1022 are prescaled by 1/4 with the
 // numerator (exact, since a resid_ok numerator is >= 2^-967).
-template <bool Fix>
+template <bool Fix, bool Bnd = false>
 __device__ __forceinline__ double div_pos_big_f(double a, double b, bool& hard) {
-  const bool z = !nz_(a);
   const double sc = hi_(b) >= 0x7FD00000u ? 0.25 : 1.0;
   const double a2 = mul(a, sc);
+  if (Bnd) {
+    const double d = lift_zero(mul(b, sc));
+    return quot_f(a2, d, rcp_f(d));
+  }
+  const bool z = !nz_(a);
   const double d = z ? 1.0 : mul(b, sc);
   double q = quot_f(a2, d, rcp_f(d));
   const bool h = !z & !(resid_ok(hi_(a2)) & normal_q(hi_(q)));
@@ -77,31 +96,46 @@ __device__ __forceinline__ double div_pos_big_f(double a, double b, bool& hard) 
 // q < 2^-28, q^2 < 2^-56 rounds away and the result is big * sqrt(1) = big
 // whatever q's last bits are.  So a hypot whose quotient is that small never
 // needs the exact path, even when q itself would be subnormal.  (A garbage
-// fast quotient -- subnormal denominator -- comes out NaN, not small.)
+// fast quotient -- subnormal denominator -- comes out NaN or inf, not
+// small.)  Since q = small / big <= 1, a quotient that matters (>= 2^-28) is
+// normal whenever the numerator passes resid_ok, so that is the whole check.
 __device__ __forceinline__ bool hypot_q_irrelevant(double q) { return hi_(q) < 0x3E300000u; }  // q < 2^-28
 
 // lanes.py:213-227 for non-negative magnitudes m1, m2 < 2^1022.
-template <bool Fix>
+template <bool Fix, bool Bnd = false>
 __device__ __forceinline__ double hypot_f(double m1, double m2, bool& hard) {
   double big, small;
   maxmin(m1, m2, big, small);
-  bool h = false;
-  double q = div_pos_f<false>(small, big, h);   // = small / max(big, TRUE_MIN)
-  h = h & !hypot_q_irrelevant(q);
+  if (Bnd) {
+    const double q = div_pos_f<false, true>(small, big, hard);
+    return mul(big, sqrt_f(fma_(q, q, 1.0)));
+  }
+  const bool z = !nz_(small);
+  const double d = z ? 1.0 : big;                   // small / max(big, TRUE_MIN), 0/0 -> 0
+  double q = quot_f(small, d, rcp_f(d));
+  const bool h = !resid_ok(hi_(small)) & !hypot_q_irrelevant(q);
   if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
   return mul(big, sqrt_f(fma_(q, q, 1.0)));
 }
 
 // lanes.py:213-227 for magnitudes < 2^1023 (complex column norms and the
 // r12 / r22 moduli, which reach 2^1022.5).
-template <bool Fix>
+template <bool Fix, bool Bnd = false>
 __device__ __forceinline__ double hypot_big_f(double m1, double m2, bool& hard) {
   double big, small;
   maxmin(m1, m2, big, small);
-  bool h = false;
-  double q = div_pos_big_f<false>(small, big, h);
-  h = h & !hypot_q_irrelevant(q);
-  if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
+  double q;
+  if (Bnd) {
+    q = div_pos_big_f<false, true>(small, big, hard);
+  } else {
+    const bool z = !nz_(small);
+    const double sc = hi_(big) >= 0x7FD00000u ? 0.25 : 1.0;
+    const double a2 = mul(small, sc);
+    const double d = z ? 1.0 : mul(big, sc);
+    q = quot_f(a2, d, rcp_f(d));
+    const bool h = !resid_ok(hi_(a2)) & !hypot_q_irrelevant(q);
+    if (Fix) { if (h) q = div_fix(small, rmax(big, kTrueMin())); } else hard |= h;
+  }
   return mul(big, sqrt_f(fma_(q, q, 1.0)));
 }
 
@@ -127,7 +161,7 @@ __device__ __forceinline__ void phase_w(double re, double im, double mag, double
   }
 }
 
-template <bool Fix>
+template <bool Fix, bool Bnd = false>
 __device__ __forceinline__ void phase_f(double re, double im, double mag, double& c, double& s, bool& hard) {
   const bool mz = !nz_(mag);
   const double sc = hi_(mag) >= 0x7FD00000u ? 0.25 : 1.0;
@@ -148,6 +182,7 @@ __device__ __forceinline__ void phase_f(double re, double im, double mag, double
   const double q2 = quot_f(a2, d, r);
   const double sq = mk_(lop_or(lop_and(hi_(q2), 0x7FFFFFFFu), lop_and(hi_(im), 0x80000000u)), lo_(q2));
   s = Fix ? (nz_(im) ? sq : im) : sq;
+  if (Bnd) return;                                 // entry phases of a bounded warp: in range
   const bool hc = nz_(a1) & !(resid_ok(hi_(a1)) & normal_q(hi_(q1)));
   const bool hs = nz_(im) & !(resid_ok(lop_and(hi_(a2), 0x7FFFFFFFu)) & normal_q(lop_and(hi_(q2), 0x7FFFFFFFu)));
   if (Fix) {
@@ -226,7 +261,7 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
 // norm is < 2^1022.5 and the pivot magnitude m11 (>= n1 / sqrt 2) lies in
 // [2^1020.5, 2^1022) unless the matrix is zero.
 // ---------------------------------------------------------------------------
-template <bool Sine, bool Fix, bool Wide = false>
+template <bool Sine, bool Fix, bool Wide = false, bool Bnd = false>
 __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   bool hard = false;
   double e[4] = {a[0], a[1], a[2], a[3]};
@@ -236,7 +271,7 @@ __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
     shift = scale_x<4>(e);
   }
   double m11 = fabs_(e[0]), m21 = fabs_(e[1]), m12 = fabs_(e[2]), m22 = fabs_(e[3]);
-  double n1 = hypot_f<Fix>(m11, m21, hard), n2 = hypot_f<Fix>(m12, m22, hard);
+  double n1 = hypot_f<Fix, Bnd>(m11, m21, hard), n2 = hypot_f<Fix, Bnd>(m12, m22, hard);
   RealUrv U;
   U.C = n1 < n2;
   swp(U.C, e[0], e[2]); swp(U.C, e[1], e[3]);
@@ -253,7 +288,7 @@ __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
     U.mt = div_den<false, Fix || kWideSub, !Fix>(m21, make_den<Fix || kWideSub>(m11), h);   // relaxed_max(., 0) is the identity here
     if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
   } else {
-    U.mt = div_pos_f<Fix>(m21, m11, hard);            // relaxed_max(., 0) is the identity here
+    U.mt = div_pos_f<Fix, Bnd>(m21, m11, hard);       // relaxed_max(., 0) is the identity here
   }
   U.cg = invsqrt_f(fma_(U.mt, U.mt, 1.0));
   const double g12 = mul(U.cg, fma_(U.mt, f22, f12));
@@ -306,7 +341,7 @@ __device__ __forceinline__ bool wide_or_sub(const double (&p)[N]) {
 // < 2^1022.5; column norms, m11 and the rotated moduli r12, r22 stay below
 // 2^1023 and use the prescaling variants.
 // ---------------------------------------------------------------------------
-template <bool Sine, bool Fix, bool Wide = false>
+template <bool Sine, bool Fix, bool Wide = false, bool Bnd = false>
 __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const double (&ai)[4], CplxOut& o) {
   bool hard = false;
   double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
@@ -317,11 +352,11 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
     shift = scale_x<8>(p);
   }
   double er[4] = {p[0], p[2], p[4], p[6]}, ei[4] = {p[1], p[3], p[5], p[7]};
-  double m11 = hypot_f<Fix>(fabs_(er[0]), fabs_(ei[0]), hard);
-  double m21 = hypot_f<Fix>(fabs_(er[1]), fabs_(ei[1]), hard);
-  double m12 = hypot_f<Fix>(fabs_(er[2]), fabs_(ei[2]), hard);
-  double m22 = hypot_f<Fix>(fabs_(er[3]), fabs_(ei[3]), hard);
-  double n1 = hypot_big_f<Fix>(m11, m21, hard), n2 = hypot_big_f<Fix>(m12, m22, hard);
+  double m11 = hypot_f<Fix, Bnd>(fabs_(er[0]), fabs_(ei[0]), hard);
+  double m21 = hypot_f<Fix, Bnd>(fabs_(er[1]), fabs_(ei[1]), hard);
+  double m12 = hypot_f<Fix, Bnd>(fabs_(er[2]), fabs_(ei[2]), hard);
+  double m22 = hypot_f<Fix, Bnd>(fabs_(er[3]), fabs_(ei[3]), hard);
+  double n1 = hypot_big_f<Fix, Bnd>(m11, m21, hard), n2 = hypot_big_f<Fix, Bnd>(m12, m22, hard);
   CplxUrv U;
   U.C = n1 < n2;
   swp(U.C, er[0], er[2]); swp(U.C, ei[0], ei[2]);
@@ -336,8 +371,8 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
     phase_w<Fix>(er[0], ei[0], m11, U.c1, U.s1, hard);
     phase_w<Fix>(er[1], ei[1], m21, U.c2, U.s2, hard);
   } else {
-    phase_f<Fix>(er[0], ei[0], m11, U.c1, U.s1, hard);
-    phase_f<Fix>(er[1], ei[1], m21, U.c2, U.s2, hard);
+    phase_f<Fix, Bnd>(er[0], ei[0], m11, U.c1, U.s1, hard);
+    phase_f<Fix, Bnd>(er[1], ei[1], m21, U.c2, U.s2, hard);
   }
   double f12r, f12i, f22r, f22i;
   cmul(U.c1, neg_(U.s1), er[2], ei[2], f12r, f12i);
@@ -347,7 +382,7 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
     U.mt = div_den<false, Fix || kWideSub, !Fix>(m21, make_den<Fix || kWideSub>(m11), h);   // m21 >= 0: relaxed_max is the identity
     if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
   } else {
-    U.mt = div_pos_big_f<Fix>(m21, m11, hard);
+    U.mt = div_pos_big_f<Fix, Bnd>(m21, m11, hard);
   }
   U.cg = invsqrt_f(fma_(U.mt, U.mt, 1.0));
   const double g12r = mul(U.cg, fma_(U.mt, f22r, f12r)), g12i = mul(U.cg, fma_(U.mt, f22i, f12i));

@@ -243,6 +243,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // CTA 0 with ordinary loads.
 // ---------------------------------------------------------------------------
 constexpr int kStages = 4;
+// Bounded (check-free) entry sites for the real fast path: valid under the
+// wide_or_sub dispatch, but measured 3 % slower on config 3 (1.50 vs 1.45 ms
+// per 2^26 lanes, memory-bound kernel), so off; the complex kernel uses them.
+#ifndef B2S_REAL_BND
+#define B2S_REAL_BND 0
+#endif
 #ifndef B2S_REAL_WIDE
 #define B2S_REAL_WIDE 2
 #endif
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
       hard = false;
     } else
 #endif
-    hard = svd2_real_f<Sine, false>(a, o);
+    hard = svd2_real_f<Sine, false, false, B2S_REAL_WIDE != 0 && B2S_REAL_BND>(a, o);
     store_real<Mode>(A, i, o);
     nh += mark_hard(A.q, hard, i);
   }
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
     if (__any_sync(0xFFFFFFFFu, wide_lane<8>(p)))
       hard = svd2_complex_f<Sine, false, true>(ar, ai, o);
     else
-      hard = svd2_complex_f<Sine, false, false>(ar, ai, o);
+      hard = svd2_complex_f<Sine, false, false, true>(ar, ai, o);   // bounded warp
     store_cplx<Mode>(A, i, o);
     nh += mark_hard(A.q, hard, i);
   }

@@ -19,10 +19,11 @@
  *
  * Device entry points are asynchronous on the given stream (cudaStream_t
  * passed as void*; NULL = legacy default stream).  Their only allocation is
- * a per-device hard-lane bit mask (4 bytes per 32 lanes, <= 256 MiB), made
- * on first use and reused;
+ * a hard-lane bit mask per (device, stream) (4 bytes per 32 lanes, <= 256
+ * MiB), made on first use of the stream and reused;
  * b2s_reserve_workspace() makes it ahead of time (e.g. before CUDA-graph
- * capture).  All are reentrant; call them from one host thread per GPU.
+ * capture).  All are reentrant: concurrent calls on different streams, or
+ * from several host threads on one stream, are safe.
  */
 #ifndef B2S_H
 #define B2S_H
@@ -162,17 +163,19 @@ int b2s_metrics(int64_t n, const double *const a_re[4],
                 double *lane_eta, void *stream);
 
 /*
- * Pre-allocate the per-device hard-lane mask for launches of up to `lanes`
- * lanes.  The fast kernels evaluate every division / sqrt with inline
- * sequences whose operand ranges the scaling phase guarantees; lanes whose
- * operands leave them (tiny ratios, subnormal entries, zero matrices) are
- * marked and recomputed with IEEE intrinsics by a fix-up kernel.
+ * Pre-allocate the hard-lane mask of `stream` on `device` for launches of up
+ * to `lanes` lanes (required before capturing launches into a CUDA graph).
+ * The fast kernels evaluate every division / sqrt with inline sequences
+ * whose operand ranges the scaling phase guarantees; lanes whose operands
+ * leave them (tiny ratios, subnormal entries, zero matrices) are marked and
+ * recomputed exactly by a fix-up kernel.
  */
-int b2s_reserve_workspace(int device, int64_t lanes);
+int b2s_reserve_workspace(int device, int64_t lanes, void *stream);
 
 /*
  * Number of hard lanes (recomputed exactly) in the most recent real or
- * complex device launch on `device`; synchronises the device.  -1 on error.
+ * complex device launch on `device` (any stream); synchronises the device.
+ * -1 on error.
  */
 long long b2s_hard_lane_count(int device);
 

@@ -61,7 +61,7 @@ def _load():
     L.b2s_synth.argtypes = [_int, ctypes.c_uint64, _i64, _i64, _PA, _PA, _P]
     L.b2s_check_fp_env.argtypes = [_int]
     L.b2s_math_probe.argtypes = [_int, _i64, _P, _P, _P, _P]
-    L.b2s_reserve_workspace.argtypes = [_int, _i64]
+    L.b2s_reserve_workspace.argtypes = [_int, _i64, _P]
     L.b2s_metrics.argtypes = [_i64, _PA, _PA, _PA, _PA, _PA, _PA, _P, _P, _P,
                               _P, _int, _P, _P, _P, _P]
     L.b2s_svd2_real_records.argtypes = [_i64, _P, _PA, _PA, _P, _P, _P, _int,

@@ -13,6 +13,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 namespace b2s {
 
@@ -639,14 +640,25 @@ static int resident_grid(K kernel, int64_t n) {
   return grid_for(kernel, kBlock, n, &err);
 }
 
-// Per-device hard-lane mask storage (4 bytes per 32 lanes of one
-// sub-launch), allocated on first use and grown on demand;
-// b2s_reserve_workspace pre-allocates (e.g. before CUDA-graph capture).
-struct Workspace {
-  std::mutex mu;
+// Hard-lane mask storage (4 bytes per 32 lanes of one sub-launch) plus the
+// launch's counter, one set per (device, stream): launches on different
+// streams may run concurrently, so they must not share it.  A launch
+// enqueues its counter reset, streaming kernel and fix-up while holding the
+// device's workspace lock, so two host threads sharing one stream cannot
+// interleave those three either.  Allocated on first use of a stream and
+// grown on demand; b2s_reserve_workspace pre-allocates (before CUDA-graph
+// capture, where allocation is not allowed).
+struct LaneQueue {
+  cudaStream_t stream;
   unsigned* mask = nullptr;
   unsigned long long* cnt = nullptr;
   size_t words = 0;
+};
+
+struct Workspace {
+  std::mutex mu;
+  std::vector<LaneQueue> queues;
+  int last = -1;                       // queue of the most recent launch
 };
 
 static Workspace& workspace(int dev) {
@@ -663,24 +675,40 @@ static bool getenv_flag(const char* name) {
   return v && *v && *v != '0';
 }
 
-static int get_queue(int64_t n, HardQueue* q) {
-  int dev = 0;
-  B2S_CUDA(cudaGetDevice(&dev));
-  Workspace& w = workspace(dev);
-  std::lock_guard<std::mutex> lock(w.mu);
+// The queue of stream `s` on the current device, large enough for n lanes.
+// Caller holds the device workspace lock.
+static int get_queue(Workspace& w, cudaStream_t s, int64_t n, HardQueue* q) {
+  int k = -1;
+  for (size_t j = 0; j < w.queues.size(); j++)
+    if (w.queues[j].stream == s) k = (int)j;
+  if (k < 0) {
+    w.queues.push_back(LaneQueue{s});
+    k = (int)w.queues.size() - 1;
+  }
+  LaneQueue& Q = w.queues[k];
   size_t want = (size_t)((n + 31) / 32);
   if (want < 4096) want = 4096;
-  if (!w.cnt) B2S_CUDA(cudaMalloc(&w.cnt, sizeof(unsigned long long)));
-  if (w.words < want) {
-    if (w.mask) cudaFree(w.mask);
-    w.mask = nullptr;
-    w.words = 0;
-    B2S_CUDA(cudaMalloc(&w.mask, want * sizeof(unsigned)));
-    w.words = want;
+  if (!Q.cnt) B2S_CUDA(cudaMalloc(&Q.cnt, sizeof(unsigned long long)));
+  if (Q.words < want) {
+    if (Q.mask) {
+      B2S_CUDA(cudaStreamSynchronize(s));          // earlier launches on s may still read it
+      cudaFree(Q.mask);
+    }
+    Q.mask = nullptr;
+    Q.words = 0;
+    B2S_CUDA(cudaMalloc(&Q.mask, want * sizeof(unsigned)));
+    Q.words = want;
   }
-  q->mask = w.mask;
-  q->cnt = w.cnt;
+  q->mask = Q.mask;
+  q->cnt = Q.cnt;
+  w.last = k;
   return 0;
+}
+
+static Workspace& current_workspace() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return workspace(dev);
 }
 
 static inline bool a16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -714,6 +742,9 @@ static int tma_grid(K kernel, size_t smem, int64_t n) {
 template <int Mode, bool Sine, bool States>
 static int launch_real(RealArgs A, cudaStream_t s) {
   const int64_t total = A.n;
+  Workspace& W = current_workspace();
+  std::unique_lock<std::mutex> lock(W.mu, std::defer_lock);
+  if (!States) lock.lock();                       // see LaneQueue
   const RealArgs base = A;
   for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
     A = base;
@@ -724,7 +755,7 @@ static int launch_real(RealArgs A, cudaStream_t s) {
     A.smax += lo; A.smin += lo; A.shift += lo;
     if (States) for (int k = 0; k < B2S_STATES_REAL; k++) A.st[k] += lo;
     if (!States) {
-      int rc = get_queue(A.n, &A.q);
+      int rc = get_queue(W, s, A.n, &A.q);
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
@@ -750,6 +781,9 @@ static int launch_real(RealArgs A, cudaStream_t s) {
 template <int Mode, bool Sine, bool States>
 static int launch_cplx(CplxArgs A, cudaStream_t s) {
   const int64_t total = A.n;
+  Workspace& W = current_workspace();
+  std::unique_lock<std::mutex> lock(W.mu, std::defer_lock);
+  if (!States) lock.lock();                       // see LaneQueue
   const CplxArgs base = A;
   for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
     A = base;
@@ -760,7 +794,7 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
     A.smax += lo; A.smin += lo; A.shift += lo;
     if (States) for (int k = 0; k < B2S_STATES_COMPLEX; k++) A.st[k] += lo;
     if (!States) {
-      int rc = get_queue(A.n, &A.q);
+      int rc = get_queue(W, s, A.n, &A.q);
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
@@ -948,14 +982,19 @@ int b2s_math_probe(int op, int64_t n, const double* a, const double* b, double* 
   return 0;
 }
 
-int b2s_reserve_workspace(int device, int64_t lanes) {
+int b2s_reserve_workspace(int device, int64_t lanes, void* stream) {
   if (lanes < 0) return fail(1, "negative lane count");
   if (lanes > kMaxLaunch) lanes = kMaxLaunch;
   int prev = 0;
   B2S_CUDA(cudaGetDevice(&prev));
   B2S_CUDA(cudaSetDevice(device));
+  Workspace& w = workspace(device);
   HardQueue q;
-  int rc = get_queue(lanes, &q);
+  int rc;
+  {
+    std::lock_guard<std::mutex> lock(w.mu);
+    rc = get_queue(w, (cudaStream_t)stream, lanes, &q);
+  }
   cudaSetDevice(prev);
   return rc;
 }
@@ -967,9 +1006,14 @@ long long b2s_hard_lane_count(int device) {
   Workspace& w = workspace(device);
   unsigned long long c = 0;
   long long out = 0;
-  if (w.cnt) {
+  unsigned long long* cnt = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(w.mu);
+    if (w.last >= 0) cnt = w.queues[w.last].cnt;
+  }
+  if (cnt) {
     if (cudaDeviceSynchronize() != cudaSuccess ||
-        cudaMemcpy(&c, w.cnt, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess)
+        cudaMemcpy(&c, cnt, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess)
       out = -1;
     else
       out = (long long)c;
@@ -1005,19 +1049,25 @@ int b2s_ring_probe(int64_t n, const double* const a[4], double* const out[11], i
 }
 
 int b2s_check_fp_env(int device) {
+  int prev = 0;
+  B2S_CUDA(cudaGetDevice(&prev));
   B2S_CUDA(cudaSetDevice(device));
-  double h_in[4] = {1.0, 0x1p-53, 0x1p-1074, 0x1p-104};
+  const double h_in[4] = {1.0, 0x1p-53, 0x1p-1074, 0x1p-104};
   double* d_in = nullptr;
   int* d_out = nullptr;
   int ok = 0;
-  B2S_CUDA(cudaMalloc(&d_in, sizeof h_in));
-  B2S_CUDA(cudaMalloc(&d_out, sizeof(int)));
-  B2S_CUDA(cudaMemcpy(d_in, h_in, sizeof h_in, cudaMemcpyHostToDevice));
-  k_fp_env<<<1, 1>>>(d_in, d_out);
-  B2S_CUDA(cudaGetLastError());
-  B2S_CUDA(cudaMemcpy(&ok, d_out, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaError_t e = cudaMalloc(&d_in, sizeof h_in);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(d_in, h_in, sizeof h_in, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_fp_env<<<1, 1>>>(d_in, d_out);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(&ok, d_out, sizeof(int), cudaMemcpyDeviceToHost);
   cudaFree(d_in);
   cudaFree(d_out);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "b2s_check_fp_env");
   return ok ? 0 : fail(7, "device FP environment check failed (rounding, gradual underflow or fma)");
 }
 

@@ -291,3 +291,68 @@ def test_sub_launch_boundaries_small_chunk_host_path():
         out, _ = b2s.run_batch(b, b2s.RunConfig(chunk=chunk))
         for k, arr in ref.trains().items():
             assert_bits_equal(out.trains()[k], arr, "%s chunk=%d" % (k, chunk))
+
+
+def _outd(out):
+    return {"u_re": list(out.u_re), "v_re": list(out.v_re),
+            "u_im": None if out.u_im is None else list(out.u_im),
+            "v_im": None if out.v_im is None else list(out.v_im),
+            "smax": out.smax, "smin": out.smin, "shift": out.shift}
+
+
+def _launch(re, im, out, stream):
+    from paper_2005_07403_b200.svd2 import launch_device
+    launch_device(re.shape[1], list(re), None if im is None else list(im), _outd(out), 0,
+                  stream=stream.cuda_stream)
+
+
+def test_concurrent_streams_keep_separate_hard_lane_queues():
+    """Launches on different streams run concurrently, each with its own
+    hard-lane mask and counter (config 4 has fix-up lanes): the results of
+    interleaved launches equal those of sequential ones."""
+    n = 1 << 19
+    batches = [synth.generate_device(4, 11 + k, k * n, n, device=DEV) for k in range(4)]
+    ref = []
+    for re, im in batches:
+        out = b2s.SvdBatchOut.empty(n, True, device=DEV)
+        _launch(re, im, out, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        ref.append(out.cpu())
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [b2s.SvdBatchOut.empty(n, True, device=DEV) for _ in batches]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for k, (re, im) in enumerate(batches):
+            _launch(re, im, outs[k], streams[k % 2])
+    torch.cuda.synchronize()
+    for k in range(len(batches)):
+        got = outs[k].cpu().trains()
+        for name, arr in ref[k].trains().items():
+            assert_bits_equal(got[name], arr, "batch %d %s" % (k, name))
+
+
+def test_cuda_graph_capture_after_reserve():
+    """With the stream's workspace reserved, a launch can be captured into a
+    CUDA graph and replayed (no allocation during capture)."""
+    n = 1 << 18
+    re, im = synth.generate_device(4, 3, 0, n, device=DEV)
+    ref = b2s.SvdBatchOut.empty(n, True, device=DEV)
+    _launch(re, im, ref, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    assert _lib.lib.b2s_reserve_workspace(0, n, s.cuda_stream) == 0
+    out = b2s.SvdBatchOut.empty(n, True, device=DEV)
+    with torch.cuda.stream(s):
+        _launch(re, im, out, s)                      # warm-up on the capture stream
+    torch.cuda.synchronize()
+    for name in ("smax", "smin", "shift"):
+        getattr(out, name).zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        _launch(re, im, out, s)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    got, want = out.cpu().trains(), ref.cpu().trains()
+    for name, arr in want.items():
+        assert_bits_equal(got[name], arr, name)

@@ -60,6 +60,12 @@ static int pipeline(int64_t n, int device, int64_t chunk, int n_in, const double
   int ndev = 0;
   B2S_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(8, "device %d out of range (have %d)", device, ndev);
+  int prev = 0;
+  B2S_CUDA(cudaGetDevice(&prev));
+  struct Restore {
+    int dev;
+    ~Restore() { cudaSetDevice(dev); }
+  } restore{prev};                                  // the caller's current device survives the call
   B2S_CUDA(cudaSetDevice(device));
   if (chunk <= 0) chunk = 1 << 22;
   chunk = (chunk + 255) / 256 * 256;

@@ -244,11 +244,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // CTA 0 with ordinary loads.
 // ---------------------------------------------------------------------------
 constexpr int kStages = 4;
-// Bounded (check-free) entry sites for the real fast path: valid under the
-// wide_or_sub dispatch, but measured 3 % slower on config 3 (1.50 vs 1.45 ms
-// per 2^26 lanes, memory-bound kernel), so off; the complex kernel uses them.
+// Bounded (check-free) entry sites for the real fast path, valid under the
+// wide_or_sub dispatch.  Short cold-clock runs of 2^26 lanes measured it 3 %
+// slower (1.50 vs 1.45 ms), but the bench workload (2^30 lanes, 20 steps,
+// power-capped at ~700 W, SM clock ~1.78 GHz) is 2.4 % faster with it
+// (43.1-43.2 vs 42.1-42.2 G SVD/s, two runs each): fewer instructions, less
+// power, higher sustained clock.
 #ifndef B2S_REAL_BND
-#define B2S_REAL_BND 0
+#define B2S_REAL_BND 1
 #endif
 #ifndef B2S_REAL_WIDE
 #define B2S_REAL_WIDE 2

@@ -39,7 +39,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
       : "memory");
 }
 
+// Blocking wait for the phase of the given parity.  B2S_MBAR_HINT_NS > 0
+// passes a suspend-time hint, so ptxas parks a waiting warp (NANOSLEEP.SYNCS,
+// woken by the barrier) instead of re-polling after the default slice.
+#ifndef B2S_MBAR_HINT_NS
+#define B2S_MBAR_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if B2S_MBAR_HINT_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity), "n"(B2S_MBAR_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -47,6 +62,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // Non-blocking probe: true once the phase of the given parity completed.

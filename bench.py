@@ -245,8 +245,41 @@ def run_device(config, world, rank, local, steps, warmup, with_quality=True):
             "clocks": clk, "launches": 2 * steps, "quality": quality}
 
 
+def pcie_bandwidth(local, nbytes=1 << 30, reps=4):
+    """Pinned host<->device copy bandwidth of this GPU's host link, both
+    directions running at once (as in the e2e pipeline), in GB/s."""
+    import torch
+    dev = torch.device("cuda", local)
+    h_src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_dst = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    res = {}
+    for rep in range(2):                    # first pass warms the link up
+        ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for k in ("h2d", "d2h")}
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(s_in):
+            ev["h2d"][0].record(s_in)
+            for _ in range(reps):
+                d_a.copy_(h_src, non_blocking=True)
+            ev["h2d"][1].record(s_in)
+        with torch.cuda.stream(s_out):
+            ev["d2h"][0].record(s_out)
+            for _ in range(reps):
+                h_dst.copy_(d_b, non_blocking=True)
+            ev["d2h"][1].record(s_out)
+        torch.cuda.synchronize(dev)
+        res = {k: nbytes * reps / (a.elapsed_time(b) * 1e-3) / 1e9 for k, (a, b) in ev.items()}
+    del h_src, h_dst, d_a, d_b
+    return res
+
+
 def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
-    """Same metric through the host-buffer C-ABI with pinned host trains."""
+    """Same metric through the host-buffer C-ABI with pinned host trains.
+    Strong-scaled like the device run: max_lanes in total, split over the
+    ranks (bounds the pinned host memory of an 8-GPU run to one copy)."""
     import torch
     import paper_2005_07403_b200 as b2s
     from paper_2005_07403_b200 import synth
@@ -254,8 +287,8 @@ def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
     n_total = cfg["n"]
     from paper_2005_07403_b200.dist import rank_span
     lo, hi = rank_span(n_total, rank, world)
-    n = min(hi - lo, max_lanes)
-    n -= n % 8
+    n = min(hi - lo, max(max_lanes // world, 1 << 20))
+    n -= n % 256
     cplx = cfg["field"] == "complex"
     pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
     # inputs: generated on the device, parked in pinned host memory
@@ -283,10 +316,20 @@ def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
     n_all = n * world
     nin = 8 if cplx else 4
     nout = 19 if cplx else 11
+    del batch, out, re, im
+    # The host link bounds this path: the step's bytes over the measured
+    # concurrent pinned-copy bandwidth of one GPU's link.
+    bw = pcie_bandwidth(local)
+    bound_s = max(n * nin * 8 / (bw["h2d"] * 1e9), n * nout * 8 / (bw["d2h"] * 1e9))
+    bound_s = max_over_ranks(bound_s, world)
     return {"value": n_all / t, "unit": UNIT, "lanes_per_step": n_all,
             "h2d_bytes_per_step": n_all * nin * 8, "d2h_bytes_per_step": n_all * nout * 8,
             "ms_per_step": t * 1e3, "path": "run_batch_into -> b2s_svd2_%s_host (pinned)"
-            % cfg["field"]}
+            % cfg["field"],
+            "roofline": {"bound": "host link (PCIe)", "h2d_gbs": round(bw["h2d"], 1),
+                         "d2h_gbs": round(bw["d2h"], 1), "bound_ms": round(bound_s * 1e3, 2),
+                         "frac": round(bound_s / t, 4),
+                         "how": "1 GiB pinned copies, both directions at once, per GPU"}}
 
 
 def roofline(res, config, hbm, how):

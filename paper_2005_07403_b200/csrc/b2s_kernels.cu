@@ -344,8 +344,14 @@ __device__ __forceinline__ double stage_val(double* st0, int v, int tid) {
   return st0[v * kBlock + tid];
 }
 
+// Resident CTAs per SM for the real streaming kernel: 3 (80 registers) and 4
+// (64 registers, 8 bytes of spills) measured equal in the bench (43.5 vs
+// 43.6 G SVD/s, two runs each) and within 1 % on configs 2 / 3.
+#ifndef B2S_REAL_MINB
+#define B2S_REAL_MINB 3
+#endif
 template <int Mode, bool Sine, bool AoS>
-__global__ void __launch_bounds__(kBlock, 3) k_svd2_real_tma(const RealArgs A) {
+__global__ void __launch_bounds__(kBlock, B2S_REAL_MINB) k_svd2_real_tma(const RealArgs A) {
   extern __shared__ __align__(128) char smem[];
   const double* src[4];
   #pragma unroll

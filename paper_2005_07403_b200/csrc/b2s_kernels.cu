@@ -677,6 +677,17 @@ static Workspace& workspace(int dev) {
 
 constexpr int64_t kMaxLaunch = int64_t(1) << 31;     // lanes per sub-launch
 
+// Lanes per sub-launch: kMaxLaunch, or B2S_MAX_LAUNCH (a multiple of 256,
+// read once) so tests can cross sub-launch boundaries with small batches.
+static int64_t max_launch() {
+  static const int64_t v = [] {
+    const char* e = getenv("B2S_MAX_LAUNCH");
+    const long long x = e ? atoll(e) : 0;
+    return (x >= 256 && x % 256 == 0 && x <= kMaxLaunch) ? (int64_t)x : kMaxLaunch;
+  }();
+  return v;
+}
+
 // Debug / A-B switches read once from the environment (e.g. B2S_NO_TMA=1
 // selects the register-prefetch streaming kernels).
 static bool getenv_flag(const char* name) {
@@ -755,9 +766,10 @@ static int launch_real(RealArgs A, cudaStream_t s) {
   std::unique_lock<std::mutex> lock(W.mu, std::defer_lock);
   if (!States) lock.lock();                       // see LaneQueue
   const RealArgs base = A;
-  for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
+  const int64_t step = max_launch();
+  for (int64_t lo = 0; lo < total; lo += step) {
     A = base;
-    A.n = (total - lo) < kMaxLaunch ? (total - lo) : kMaxLaunch;
+    A.n = (total - lo) < step ? (total - lo) : step;
     for (int t = 0; t < 4; t++) { A.u[t] += lo; A.v[t] += lo; }
     if (A.aos) A.a[0] += lo * 4;                 // 32 doubles per 8 lanes
     else for (int t = 0; t < 4; t++) A.a[t] += lo;
@@ -794,9 +806,10 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
   std::unique_lock<std::mutex> lock(W.mu, std::defer_lock);
   if (!States) lock.lock();                       // see LaneQueue
   const CplxArgs base = A;
-  for (int64_t lo = 0; lo < total; lo += kMaxLaunch) {
+  const int64_t step = max_launch();
+  for (int64_t lo = 0; lo < total; lo += step) {
     A = base;
-    A.n = (total - lo) < kMaxLaunch ? (total - lo) : kMaxLaunch;
+    A.n = (total - lo) < step ? (total - lo) : step;
     for (int t = 0; t < 4; t++) { A.ur[t] += lo; A.ui[t] += lo; A.vr[t] += lo; A.vi[t] += lo; }
     if (A.aos) A.ar[0] += lo * 8;                // 64 doubles per 8 lanes
     else for (int t = 0; t < 4; t++) { A.ar[t] += lo; A.ai[t] += lo; }

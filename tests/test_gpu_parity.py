@@ -5,6 +5,8 @@ public API.  Ground truth is the reference's own output (tests/golden/,
 made by running lanesvd) and, for arbitrary inputs, the oracle pinned to it.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -392,3 +394,39 @@ def test_stress_configs_every_kernel_path(config, path):
                       backscale_mode=mode, sine_form=sine)
     for name, arr in ref.trains().items():
         assert_bits_equal(got[name], arr[..., :n], "config %d %s %s" % (config, path, name))
+
+
+_SUBLAUNCH_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle, paper_2005_07403_b200 as b2s
+from paper_2005_07403_b200 import synth, records as R
+from paper_2005_07403_b200.layout import from_trains
+n = 3 * 65536 + 1000
+for config in (2, 4):
+    re, im = synth.generate(config, 23, 5000, n)
+    ref = oracle.svd2(re, im).trains()
+    b = from_trains(re, im).to("cuda")
+    out, _ = b2s.run_batch(b, b2s.RunConfig(field=b.field))
+    rec = R.run_records(R.trains_to_records(re, im), n, b.field).cpu().trains()
+    for name, got in (("trains", out.cpu().trains()), ("records", rec)):
+        for k, arr in ref.items():
+            g = np.ascontiguousarray(got[k][..., :n]).view(np.uint64)
+            if not np.array_equal(g, np.ascontiguousarray(arr).view(np.uint64)):
+                print("MISMATCH config %d %s %s" % (config, name, k)); sys.exit(1)
+print("OK")
+"""
+
+
+def test_sub_launch_split_on_device():
+    """Device batches larger than one sub-launch (B2S_MAX_LAUNCH forces
+    65 536-lane sub-launches: 3 full ones and a ragged fourth with a
+    sub-tile tail) through the SoA and AoSoA-8 kernels, configs 2 and 4
+    (fix-up lanes in several sub-launches): bit-identical to the oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, B2S_MAX_LAUNCH="65536")
+    r = subprocess.run([sys.executable, "-c", _SUBLAUNCH_SCRIPT, root], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr

@@ -161,12 +161,16 @@ __device__ __forceinline__ void phase_w(double re, double im, double mag, double
   }
 }
 
+// (d_out, r_out: the prescaled denominator and its reciprocal, for a caller
+// dividing something else by the same mag.)
 template <bool Fix, bool Bnd = false>
-__device__ __forceinline__ void phase_f(double re, double im, double mag, double& c, double& s, bool& hard) {
+__device__ __forceinline__ void phase_f(double re, double im, double mag, double& c, double& s, bool& hard,
+                                        double* d_out = nullptr, double* r_out = nullptr) {
   const bool mz = !nz_(mag);
   const double sc = hi_(mag) >= 0x7FD00000u ? 0.25 : 1.0;
   const double d = mz ? 1.0 : mul(mag, sc);
   const double r = rcp_f(d);
+  if (d_out) { *d_out = d; *r_out = r; }
   // A zero part gives an exactly zero quotient (0 / mag); it is selected
   // directly so that a garbage reciprocal (subnormal mag, flagged through
   // the other part) can never leak through it.
@@ -195,7 +199,7 @@ __device__ __forceinline__ void phase_f(double re, double im, double mag, double
 
 // svd2.py:306-343.  r11 = 0 or r11 in [2^1021, 2^1022.5] (the norm of the
 // pivot column, which holds the scaled maximum entry); 0 <= r12, r22 <= r11.
-template <bool Fix, bool Wide = false>
+template <bool Fix, bool Wide = false, bool Lean = !Fix>
 __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bool& hard) {
   double qx, qy;
   bool hx = false, hy = false;
@@ -222,7 +226,10 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
   } else {
     hard |= hx | hy;
   }
-  const double x = rmax(qx, 0.0), y = rmax(qy, 0.0);
+  // relaxed_max(q, 0) (svd2.py:324-325): q >= +0 whenever r11 > 0, which
+  // holds on every lane the streaming kernel keeps (a zero matrix is flagged
+  // hard by scale_f); r11 = 0 (0 / 0) only reaches the exact re-evaluation.
+  const double x = Lean ? qx : rmax(qx, 0.0), y = Lean ? qy : rmax(qy, 0.0);
   double hi, lo;
   maxmin(x, y, hi, lo);
   const double num = mul(mul(lo, 2.0), hi);                  // scalef(min, 1) * max
@@ -261,6 +268,9 @@ __device__ __forceinline__ Tri triangle_f(double r11, double r12, double r22, bo
 // norm is < 2^1022.5 and the pivot magnitude m11 (>= n1 / sqrt 2) lies in
 // [2^1020.5, 2^1022) unless the matrix is zero.
 // ---------------------------------------------------------------------------
+#ifndef B2S_REAL_LEAN
+#define B2S_REAL_LEAN 1   // bench (power-capped): +1.2 % (43.9 vs 43.3 G SVD/s); cold 2^26: -0.5 %
+#endif
 template <bool Sine, bool Fix, bool Wide = false, bool Bnd = false>
 __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   bool hard = false;
@@ -296,7 +306,7 @@ __device__ __forceinline__ bool svd2_real_f(const double (&a)[4], RealOut& o) {
   U.dt = sgn_(g12);
   const double w = xor_(g22, U.dt);
   U.dh = sgn_(w);
-  const Tri T = triangle_f<Fix, Wide>(r11, fabs_(g12), fabs_(w), hard);
+  const Tri T = triangle_f<Fix, Wide, B2S_REAL_LEAN && !Fix>(r11, fabs_(g12), fabs_(w), hard);
   assemble_real<Sine>(U, T, o);
   o.shift = shift;
   return hard;
@@ -358,6 +368,7 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
   double m22 = hypot_f<Fix, Bnd>(fabs_(er[3]), fabs_(ei[3]), hard);
   double n1 = hypot_big_f<Fix, Bnd>(m11, m21, hard), n2 = hypot_big_f<Fix, Bnd>(m12, m22, hard);
   CplxUrv U;
+  double d11 = 1.0, r11p = 1.0;             // e11's phase denominator m11 * sc and its reciprocal
   U.C = n1 < n2;
   swp(U.C, er[0], er[2]); swp(U.C, ei[0], ei[2]);
   swp(U.C, er[1], er[3]); swp(U.C, ei[1], ei[3]);
@@ -371,7 +382,7 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
     phase_w<Fix>(er[0], ei[0], m11, U.c1, U.s1, hard);
     phase_w<Fix>(er[1], ei[1], m21, U.c2, U.s2, hard);
   } else {
-    phase_f<Fix, Bnd>(er[0], ei[0], m11, U.c1, U.s1, hard);
+    phase_f<Fix, Bnd>(er[0], ei[0], m11, U.c1, U.s1, hard, &d11, &r11p);
     phase_f<Fix, Bnd>(er[1], ei[1], m21, U.c2, U.s2, hard);
   }
   double f12r, f12i, f22r, f22i;
@@ -381,6 +392,13 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
     bool h = false;
     U.mt = div_den<false, Fix || kWideSub, !Fix>(m21, make_den<Fix || kWideSub>(m11), h);   // m21 >= 0: relaxed_max is the identity
     if (Fix) { if (h) U.mt = div_fix(m21, m11); } else hard |= h;
+  } else if (!Fix) {
+    // m21 / m11 with the reciprocal e11's phase formed: on every lane the
+    // streaming kernel keeps (m11 > 0) its denominator is m11 * sc, exactly
+    // div_pos_big_f's.  m21 <= m11, so the quotient is <= 1.
+    const double a2 = mul(m21, hi_(m11) >= 0x7FD00000u ? 0.25 : 1.0);
+    U.mt = quot_f(a2, d11, r11p);
+    if (!Bnd) hard |= nz_(m21) & !(resid_ok(hi_(a2)) & normal_q(hi_(U.mt)));
   } else {
     U.mt = div_pos_big_f<Fix, Bnd>(m21, m11, hard);
   }

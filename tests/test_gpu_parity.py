@@ -430,3 +430,49 @@ def test_sub_launch_split_on_device():
     r = subprocess.run([sys.executable, "-c", _SUBLAUNCH_SCRIPT, root], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr
+
+
+def _random_finite(rng, count):
+    """Uniform 64-bit patterns with non-finite ones redrawn: the whole
+    magnitude range, subnormals and both zero signs (the fuzz corpus of the
+    reference's acceptance suite, test_acceptance.py:70-101)."""
+    vals = rng.integers(0, 2 ** 64, size=count, dtype=np.uint64).view(np.float64)
+    bad = ~np.isfinite(vals)
+    while bad.any():
+        vals[bad] = rng.integers(0, 2 ** 64, size=int(bad.sum()), dtype=np.uint64).view(np.float64)
+        bad = ~np.isfinite(vals)
+    return vals
+
+
+@pytest.mark.parametrize("field", ["real", "complex"])
+def test_theorem1_invariants_full_range_fuzz(field):
+    """test_acceptance.py:115-140 on 2^20 full-bit-pattern lanes per field:
+    scaled singular values finite, sorted and non-negative; |tan psi| <=
+    sqrt(2)(1 + 2 eps53); |tan psi| >= |tan phi|; cos psi >= (1 - 2 eps53)
+    / sqrt(3); every factor finite -- on the streaming kernels' outputs and
+    the state dump, which must agree bit for bit."""
+    eps = 2.0 ** -53
+    n = 1 << 20
+    rng = np.random.default_rng(2026 if field == "real" else 2027)
+    ntr = 4 if field == "real" else 8
+    parts = tuple(torch.from_numpy(_random_finite(rng, n)).to(DEV) for _ in range(ntr))
+    svd, st = b2s.svd2_lanes(parts, with_states=True)
+    re = torch.stack(parts[0::2] if ntr == 8 else parts)
+    im = torch.stack(parts[1::2]) if ntr == 8 else None
+    fast, _ = b2s.run_batch(b2s.Batch2x2(n=n, re=re, im=im), b2s.RunConfig(field=field))
+    smax, smin = fast.smax.cpu().numpy(), fast.smin.cpu().numpy()
+    assert_bits_equal(smax, svd.smax_scaled.cpu().numpy(), "smax fast vs state-dump kernel")
+    assert_bits_equal(smin, svd.smin_scaled.cpu().numpy(), "smin fast vs state-dump kernel")
+    assert np.isfinite(smax).all() and np.isfinite(smin).all()
+    assert (smax >= smin).all() and (smin >= 0.0).all()
+    lt = st["left_tan"].cpu().numpy()
+    rt = st["right_tan"].cpu().numpy()
+    assert (np.abs(rt) <= np.sqrt(2.0) * (1 + 2 * eps)).all()
+    assert (np.abs(rt) >= np.abs(lt)).all()
+    # cos psi is V's (1,1) entry before the column swap (svd2.py:350-369)
+    swap_c = st["swap_cols"].cpu().numpy() != 0
+    v11, v21 = np.abs(svd.v11[0].cpu().numpy()), np.abs(svd.v21[0].cpu().numpy())
+    rc = np.where(swap_c, v21, v11)
+    assert (rc >= (1 / np.sqrt(3.0)) * (1 - 2 * eps)).all()
+    for t in list(fast.u_re) + list(fast.v_re) + ([] if im is None else list(fast.u_im) + list(fast.v_im)):
+        assert torch.isfinite(t).all()

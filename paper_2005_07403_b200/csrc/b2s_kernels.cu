@@ -131,6 +131,29 @@ __device__ __forceinline__ void load_cplx(const CplxArgs& A, int64_t i, double (
   }
 }
 
+// The same with evict-first streaming loads (the LDG streaming kernels).
+__device__ __forceinline__ void load_real_cs(const RealArgs& A, int64_t i, double (&a)[4]) {
+  if (A.aos) {
+    const double* r = A.a[0] + (i >> 3) * 32 + (i & 7);
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = ld_stream(r + 8 * t);
+  } else {
+    #pragma unroll
+    for (int t = 0; t < 4; t++) a[t] = ld_stream(A.a[t] + i);
+  }
+}
+
+__device__ __forceinline__ void load_cplx_cs(const CplxArgs& A, int64_t i, double (&ar)[4], double (&ai)[4]) {
+  if (A.aos) {
+    const double* r = A.ar[0] + (i >> 3) * 64 + (i & 7);
+    #pragma unroll
+    for (int t = 0; t < 4; t++) { ar[t] = ld_stream(r + 16 * t); ai[t] = ld_stream(r + 16 * t + 8); }
+  } else {
+    #pragma unroll
+    for (int t = 0; t < 4; t++) { ar[t] = ld_stream(A.ar[t] + i); ai[t] = ld_stream(A.ai[t] + i); }
+  }
+}
+
 // A marked lane again, with every failing call site re-evaluated exactly.
 template <int Mode, bool Sine>
 __device__ __forceinline__ void redo_real(const RealArgs& A, int64_t i) {
@@ -177,15 +200,11 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= A.n) return;
   double nx[4];
-  #pragma unroll
-  for (int t = 0; t < 4; t++) nx[t] = ld_stream(A.a[t] + i);
+  load_real_cs(A, i, nx);
   for (; i < A.n; i += stride) {
     double a[4] = {nx[0], nx[1], nx[2], nx[3]};
     const int64_t j = i + stride;
-    if (j < A.n) {
-      #pragma unroll
-      for (int t = 0; t < 4; t++) nx[t] = ld_stream(A.a[t] + j);
-    }
+    if (j < A.n) load_real_cs(A, j, nx);
     RealOut o;
     if (States) {
       LaneStates s;
@@ -208,16 +227,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   if (i >= A.n) return;
   double nr[4], ni[4];
-  #pragma unroll
-  for (int t = 0; t < 4; t++) { nr[t] = ld_stream(A.ar[t] + i); ni[t] = ld_stream(A.ai[t] + i); }
+  load_cplx_cs(A, i, nr, ni);
   for (; i < A.n; i += stride) {
     double ar[4] = {nr[0], nr[1], nr[2], nr[3]};
     double ai[4] = {ni[0], ni[1], ni[2], ni[3]};
     const int64_t j = i + stride;
-    if (j < A.n) {
-      #pragma unroll
-      for (int t = 0; t < 4; t++) { nr[t] = ld_stream(A.ar[t] + j); ni[t] = ld_stream(A.ai[t] + j); }
-    }
+    if (j < A.n) load_cplx_cs(A, j, nr, ni);
     CplxOut o;
     if (States) {
       LaneStates s;
@@ -244,6 +259,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // CTA 0 with ordinary loads.
 // ---------------------------------------------------------------------------
 constexpr int kStages = 4;
+// The sub-tile tail (n mod 256 lanes): 1 = processed by CTA 0 of the TMA
+// kernel with ordinary loads, 0 = a separate one-CTA launch of the LDG
+// kernel (keeps another copy of the pipeline out of the TMA kernel).
+// Measured per 2^26 lanes: real 0 is 3 % faster on config 2 and equal on
+// config 3 (and in the bench); complex 0 is 0.3-0.6 % slower on configs 1
+// and 4.  The LDG kernels read AoSoA-8 records too, for record tails.
+#ifndef B2S_TMA_TAIL_REAL
+#define B2S_TMA_TAIL_REAL 0
+#endif
+#ifndef B2S_TMA_TAIL_CPLX
+#define B2S_TMA_TAIL_CPLX 1
+#endif
 // Bounded (check-free) entry sites for the real fast path, valid under the
 // wide_or_sub dispatch.  Short cold-clock runs of 2^26 lanes measured it 3 %
 // slower (1.50 vs 1.45 ms), but the bench workload (2^30 lanes, 20 steps,
@@ -390,7 +417,7 @@ __global__ void __launch_bounds__(kBlock, B2S_REAL_MINB) k_svd2_real_tma(const R
     store_real<Mode>(A, i, o);
     nh += mark_hard(A.q, hard, i);
   }
-  if (blockIdx.x == 0) {
+  if (B2S_TMA_TAIL_REAL && blockIdx.x == 0) {
     const int64_t i = tiles * kBlock + tid;
     if (i < A.n) {
       double a[4];
@@ -446,7 +473,7 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
     store_cplx<Mode>(A, i, o);
     nh += mark_hard(A.q, hard, i);
   }
-  if (blockIdx.x == 0) {
+  if (B2S_TMA_TAIL_CPLX && blockIdx.x == 0) {
     const int64_t i = tiles * kBlock + tid;
     if (i < A.n) {
       double ar[4], ai[4];
@@ -795,6 +822,17 @@ static int launch_real(RealArgs A, cudaStream_t s) {
       const size_t sm = TmaRing<4>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
+      const int64_t head = A.n / kBlock * kBlock;
+      if (!B2S_TMA_TAIL_REAL && head < A.n) {
+        RealArgs T = A;
+        T.n = A.n - head;
+        for (int t = 0; t < 4; t++) { T.u[t] += head; T.v[t] += head; }
+        if (T.aos) T.a[0] += head * 4;
+        else for (int t = 0; t < 4; t++) T.a[t] += head;
+        T.smax += head; T.smin += head; T.shift += head;
+        T.q.mask += head >> 5;
+        k_svd2_real<Mode, Sine, false><<<1, kBlock, 0, s>>>(T);
+      }
     } else {
       auto k = k_svd2_real<Mode, Sine, States>;
       k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);
@@ -835,6 +873,17 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
       const size_t sm = TmaRing<8>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
+      const int64_t head = A.n / kBlock * kBlock;
+      if (!B2S_TMA_TAIL_CPLX && head < A.n) {
+        CplxArgs T = A;
+        T.n = A.n - head;
+        for (int t = 0; t < 4; t++) { T.ur[t] += head; T.ui[t] += head; T.vr[t] += head; T.vi[t] += head; }
+        if (T.aos) T.ar[0] += head * 8;
+        else for (int t = 0; t < 4; t++) { T.ar[t] += head; T.ai[t] += head; }
+        T.smax += head; T.smin += head; T.shift += head;
+        T.q.mask += head >> 5;
+        k_svd2_complex<Mode, Sine, false><<<1, kBlock, 0, s>>>(T);
+      }
     } else {
       auto k = k_svd2_complex<Mode, Sine, States>;
       k<<<resident_grid(k, A.n), kBlock, 0, s>>>(A);

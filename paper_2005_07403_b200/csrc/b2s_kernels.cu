@@ -2,10 +2,12 @@
 // points (include/b2s.h).
 //
 // K1 real / K2 complex: one SVD per thread, the whole pipeline fused in
-// registers; SoA trains streamed with coalesced evict-first loads/stores.
-// A resident grid (SMs x CTAs/SM) walks the batch with a grid stride and
-// prefetches the next lane's inputs before computing the current one, so
-// every thread keeps one lane of loads in flight behind its arithmetic.
+// registers; SoA trains streamed with coalesced evict-first stores.  The
+// default kernels (k_svd2_*_tma) stage their inputs through a TMA ring in
+// shared memory; the LDG kernels (k_svd2_real / k_svd2_complex: a resident
+// grid-stride loop that prefetches the next lane's inputs into registers)
+// serve misaligned trains, state dumps and the real kernel's sub-tile tail.
+// K1f / K2f (k_fix_*) recompute the lanes a streaming kernel flagged.
 #include "../../include/b2s.h"
 #include "b2s_common.cuh"
 #include "b2s_fast.cuh"
@@ -255,8 +257,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // stage's mbarrier and issues one cp.async.bulk per input train; the loads
 // of the next kStages-1 tiles are in flight while the CTA computes the
 // current one.  Outputs go straight from registers with streaming stores
-// (coalesced 256 B per warp per train).  The sub-tile tail is processed by
-// CTA 0 with ordinary loads.
+// (coalesced 256 B per warp per train).  The sub-tile tail (n mod 256
+// lanes) is processed by CTA 0 with ordinary loads (complex) or by a
+// one-CTA launch of the LDG kernel (real), see B2S_TMA_TAIL_*.
 // ---------------------------------------------------------------------------
 constexpr int kStages = 4;
 // The sub-tile tail (n mod 256 lanes): 1 = processed by CTA 0 of the TMA

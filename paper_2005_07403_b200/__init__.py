@@ -1,29 +1,29 @@
-"""B200-native batched SVD of 2x2 real and complex fp64 matrices.
+"""paper_2005_07403_b200 -- batched 2x2 SVDs (real and complex fp64) on B200.
 
-A from-scratch GPU engine for the batched algorithm of arXiv 2005.07403
-(Novakovic), exposing the API of the reference package ``lanesvd`` 0.1.0:
-exact power-of-two prescaling, URV reduction to a non-negative triangle,
-closed-form triangle SVD and U/V assembly, fused in one sm_100a kernel per
-field that runs one SVD per thread over structure-of-arrays trains.
-Results are bit-identical to the reference's CPU pipeline.
+The hot path of ``lanesvd`` 0.1.0 (arXiv 2005.07403), rebuilt as sm_100a
+CUDA behind the reference's own Python API and SoA layout: exact
+power-of-two prescaling, URV reduction to a non-negative triangle, the
+closed-form triangle SVD and the U/V assembly run fused in one kernel per
+field, one matrix per thread, with results bit-identical to the reference.
 
-The native library ``_native/libb2s.so`` (C-ABI: ``include/b2s.h``) is the
-only compute path; importing this package without it raises.
+Compute happens only in ``_native/libb2s.so`` (C ABI: ``include/b2s.h``);
+without it this import fails -- there is no CPU path.
 """
 
 from ._lib import LIB_PATH, assert_device_fp_env
-from .layout import (LANE_WIDTH, Batch2x2, MatrixSvd, SvdBatchOut,
-                     aligned_zeros, from_trains, pack, padded_len, unpack,
-                     unpack_inputs)
-from .driver import (RunConfig, run_batch, run_batch_into, shards,
-                     svd2_chunk, svd2_single)
+from .driver import RunConfig, run_batch, run_batch_into, shards, svd2_chunk, svd2_single
+from .layout import (LANE_WIDTH, Batch2x2, MatrixSvd, SvdBatchOut, aligned_zeros,
+                     from_trains, pack, padded_len, unpack, unpack_inputs)
 from .svd2 import Svd2, backscale, svd2_lanes
+from .verify import Metrics, metrics
 
-__all__ = [
-    "LANE_WIDTH", "padded_len", "aligned_zeros", "Batch2x2", "SvdBatchOut",
-    "MatrixSvd", "pack", "unpack", "from_trains", "unpack_inputs",
-    "RunConfig", "run_batch", "run_batch_into", "svd2_chunk", "svd2_single", "shards",
-    "Svd2", "svd2_lanes", "backscale", "assert_device_fp_env", "LIB_PATH",
-]
+# lanesvd's package namespace (lanesvd/__init__.py) plus this engine's extras
+__all__ = sorted([
+    "LANE_WIDTH", "padded_len", "Batch2x2", "SvdBatchOut", "MatrixSvd",
+    "RunConfig", "run_batch", "svd2_chunk", "svd2_single", "Metrics", "metrics",
+    "aligned_zeros", "pack", "unpack", "unpack_inputs", "from_trains",
+    "run_batch_into", "shards", "Svd2", "svd2_lanes", "backscale",
+    "assert_device_fp_env", "LIB_PATH",
+])
 
 __version__ = "0.1.0"

@@ -1,15 +1,15 @@
-"""Structure-of-arrays batch containers (drop-in for lanesvd.layout).
+"""Batch containers for the SoA trains (drop-in for lanesvd.layout).
 
-Same layout contract as the reference (layout.py:1-16): a batch of n
-matrices is a C-contiguous (4, n_hat) float64 array whose rows are the
-entry trains e11, e21, e12, e22 (column-major entry order); complex batches
-carry a second (4, n_hat) array of imaginary parts.  n_hat = ceil(n/8)*8 and
-padding lanes hold zeros, which decompose as zero matrices (sigma 0,
-shift DBL_MAX, U = V = I).
+The contract is the reference's (layout.py:1-16): n matrices live in a
+C-contiguous (4, n_hat) float64 block whose rows are the entry trains in
+column-major entry order -- e11, e21, e12, e22 -- with lane k of every row
+belonging to matrix k; a complex batch carries a second block of imaginary
+parts.  n_hat = ceil(n / 8) * 8, and padding lanes are zeros (they come out
+as zero-matrix results: sigma 0, shift DBL_MAX, U = V = I).
 
-B200 additions: trains may live in HBM as CUDA ``torch.Tensor`` objects
-(``Batch2x2.to(device)``); host trains are 64-byte aligned NumPy arrays
-exactly as in the reference, and the host path streams them through the GPU.
+On B200 the blocks may also be CUDA tensors resident in HBM
+(``Batch2x2.to(device)``, ``SvdBatchOut.empty(..., device=...)``); host
+blocks are 64-byte aligned NumPy arrays, as the reference allocates them.
 """
 
 from __future__ import annotations
@@ -25,28 +25,32 @@ __all__ = [
     "is_device_array",
 ]
 
-LANE_WIDTH = 8            # lanes.py:38; n_hat granularity
-_ALIGN = 64
-_ENTRY_ORDER = ((0, 0), (1, 0), (0, 1), (1, 1))   # e11, e21, e12, e22
+LANE_WIDTH = 8                  # lanes.py:38: batches are whole 8-lane chunks
+ROW_ALIGN_BYTES = 64
+# train t holds matrix entry ENTRIES[t] = (row, col)
+ENTRIES = ((0, 0), (1, 0), (0, 1), (1, 1))
 
 
 def padded_len(n):
-    """Smallest multiple of LANE_WIDTH >= n (layout.py:33-37)."""
+    """n rounded up to a whole number of LANE_WIDTH-lane chunks
+    (layout.py:33-37); ValueError for n < 0."""
     n = int(n)
     if n < 0:
         raise ValueError("negative batch size")
-    return (n + LANE_WIDTH - 1) // LANE_WIDTH * LANE_WIDTH
+    chunks, rest = divmod(n, LANE_WIDTH)
+    return (chunks + (rest > 0)) * LANE_WIDTH
 
 
 def aligned_zeros(rows, cols):
-    """Zeroed C-contiguous (rows, cols) float64 host array whose rows all
-    start on a 64-byte boundary (layout.py:40-51)."""
+    """(rows, cols) float64 zeros, C order, every row on a 64-byte boundary
+    (layout.py:40-51): the block starts aligned and a row is a whole number
+    of 8-double chunks."""
     if cols % LANE_WIDTH:
         raise ValueError("column count must be a multiple of %d" % LANE_WIDTH)
-    count = rows * cols
-    raw = np.zeros(count + _ALIGN // 8, dtype=np.float64)
-    skip = ((-raw.ctypes.data) % _ALIGN) // 8
-    return raw[skip:skip + count].reshape(rows, cols)
+    slack = ROW_ALIGN_BYTES // 8
+    store = np.zeros(rows * cols + slack, dtype=np.float64)
+    lead = (-store.ctypes.data % ROW_ALIGN_BYTES) // 8
+    return store[lead:lead + rows * cols].reshape(rows, cols)
 
 
 def is_device_array(x):
@@ -54,19 +58,18 @@ def is_device_array(x):
     return getattr(x, "is_cuda", False) is True
 
 
-def _device_zeros(shape, device):
-    import torch
-    return torch.zeros(shape, dtype=torch.float64, device=device)
-
-
-def _device_empty(shape, device):
+def _hbm_block(shape, device):
     import torch
     return torch.empty(shape, dtype=torch.float64, device=device)
 
 
+def _to_host(x):
+    return None if x is None else (x.cpu().numpy() if is_device_array(x) else x)
+
+
 class MatrixSvd(NamedTuple):
-    """One unpacked result (layout.py:54-66): u, v (2, 2) arrays and the
-    stored smax, smin, shift lane values."""
+    """One matrix's result (layout.py:54-66): U, V as (2, 2) arrays and the
+    lane's stored smax, smin, shift."""
     u: np.ndarray
     v: np.ndarray
     smax: float
@@ -74,28 +77,29 @@ class MatrixSvd(NamedTuple):
     shift: float
 
 
+def _check_blocks(n, re, im):
+    shape = tuple(re.shape)
+    well_formed = len(shape) == 2 and shape[0] == 4 and shape[1] % LANE_WIDTH == 0
+    if not well_formed:
+        raise ValueError("trains must be (4, multiple of %d), got %r" % (LANE_WIDTH, shape))
+    if im is not None and tuple(im.shape) != shape:
+        raise ValueError("re/im train shapes differ")
+    if im is not None and is_device_array(im) != is_device_array(re):
+        raise ValueError("re/im trains must both be host or device")
+    if n < 0 or n > shape[1]:
+        raise ValueError("n outside the padded train length")
+
+
 @dataclass
 class Batch2x2:
-    """Input batch: n genuine lanes inside (4, n_hat) trains (layout.py:69-103).
-
-    ``re``/``im`` are host NumPy arrays or CUDA tensors (both the same kind).
-    """
+    """An input batch: ``n`` genuine lanes in (4, n_hat) train blocks
+    (layout.py:69-103).  ``re``/``im``: host arrays or CUDA tensors."""
     n: int
     re: object
     im: object = None
 
     def __post_init__(self):
-        shape = tuple(self.re.shape)
-        if len(shape) != 2 or shape[0] != 4 or shape[1] % LANE_WIDTH:
-            raise ValueError("trains must be (4, multiple of %d), got %r"
-                             % (LANE_WIDTH, shape))
-        if self.im is not None:
-            if tuple(self.im.shape) != shape:
-                raise ValueError("re/im train shapes differ")
-            if is_device_array(self.im) != is_device_array(self.re):
-                raise ValueError("re/im trains must both be host or device")
-        if not 0 <= self.n <= shape[1]:
-            raise ValueError("n outside the padded train length")
+        _check_blocks(self.n, self.re, self.im)
 
     @property
     def n_hat(self):
@@ -103,44 +107,48 @@ class Batch2x2:
 
     @property
     def field(self):
-        return "real" if self.im is None else "complex"
+        return "complex" if self.im is not None else "real"
 
     @property
     def on_device(self):
         return is_device_array(self.re)
 
     def parts(self):
-        """Component trains in kernel order (re/im interleaved per entry)."""
-        if self.im is None:
-            return tuple(self.re[t] for t in range(4))
-        return tuple(x for t in range(4) for x in (self.re[t], self.im[t]))
+        """The component trains in kernel order: e11, e21, e12, e22, or for
+        complex batches e11re, e11im, e21re, ... (svd2.py:521-570)."""
+        blocks = (self.re,) if self.im is None else (self.re, self.im)
+        return tuple(b[t] for t in range(4) for b in blocks)
 
     def to(self, device):
-        """Copy the trains into HBM on ``device`` (bit-exact)."""
+        """A copy with both blocks in HBM on ``device`` (bit-exact)."""
         import torch
 
-        def mv(a):
-            if not is_device_array(a):
-                a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-            return a.to(device=device, dtype=torch.float64).contiguous()
-        return Batch2x2(n=self.n, re=mv(self.re),
-                        im=None if self.im is None else mv(self.im))
+        def upload(block):
+            t = block if is_device_array(block) else torch.from_numpy(
+                np.ascontiguousarray(block, dtype=np.float64))
+            return t.to(device=device, dtype=torch.float64).contiguous()
+        return Batch2x2(self.n, upload(self.re), None if self.im is None else upload(self.im))
 
     def cpu(self):
+        """A host copy in aligned blocks (self when already on the host)."""
         if not self.on_device:
             return self
-        re = aligned_zeros(4, self.n_hat)
-        re[:] = self.re.cpu().numpy()
-        im = None
-        if self.im is not None:
-            im = aligned_zeros(4, self.n_hat)
-            im[:] = self.im.cpu().numpy()
-        return Batch2x2(n=self.n, re=re, im=im)
+
+        def download(block):
+            host = aligned_zeros(4, self.n_hat)
+            np.copyto(host, block.cpu().numpy())
+            return host
+        return Batch2x2(self.n, download(self.re), None if self.im is None else download(self.im))
+
+
+_OUT_NAMES = ("u_re", "u_im", "v_re", "v_im", "smax", "smin", "shift")
 
 
 @dataclass
 class SvdBatchOut:
-    """Output batch, same layout as the input (layout.py:106-130)."""
+    """Output trains in the input's layout (layout.py:106-130): U and V as
+    (4, n_hat) blocks (imaginary blocks None for real batches), smax, smin
+    and shift as (n_hat,) vectors."""
     n: int
     u_re: object
     u_im: object
@@ -160,118 +168,107 @@ class SvdBatchOut:
 
     @classmethod
     def empty(cls, n, complex_field, device=None):
-        """Allocate output trains: aligned host arrays, or HBM tensors when
-        ``device`` names a CUDA device (uninitialised; every lane is written)."""
+        """Output storage for n lanes: zeroed aligned host blocks, or
+        uninitialised HBM tensors on ``device`` (every lane is written)."""
         n_hat = padded_len(n)
         if device is None:
-            mk = lambda: aligned_zeros(4, n_hat)
-            vec = lambda: aligned_zeros(1, n_hat)[0]
+            block = lambda: aligned_zeros(4, n_hat)
+            vector = lambda: aligned_zeros(1, n_hat)[0]
         else:
-            mk = lambda: _device_empty((4, n_hat), device)
-            vec = lambda: _device_empty((n_hat,), device)
-        return cls(n=n, u_re=mk(), u_im=mk() if complex_field else None,
-                   v_re=mk(), v_im=mk() if complex_field else None,
-                   smax=vec(), smin=vec(), shift=vec())
+            block = lambda: _hbm_block((4, n_hat), device)
+            vector = lambda: _hbm_block((n_hat,), device)
+        cplx = bool(complex_field)
+        return cls(n, block(), block() if cplx else None, block(), block() if cplx else None,
+                   vector(), vector(), vector())
 
     def trains(self):
-        """Named output trains (u/v blocks are (4, n_hat))."""
-        out = {"u_re": self.u_re, "v_re": self.v_re, "smax": self.smax,
-               "smin": self.smin, "shift": self.shift}
-        if self.u_im is not None:
-            out["u_im"] = self.u_im
-            out["v_im"] = self.v_im
-        return out
+        """Output trains by name; the imaginary blocks only when present."""
+        return {k: getattr(self, k) for k in _OUT_NAMES if getattr(self, k) is not None}
 
     def cpu(self):
-        """Host copy (NumPy) of a device-resident result."""
+        """Host (NumPy) copy of a device-resident result."""
         if not self.on_device:
             return self
-        cv = lambda a: None if a is None else a.cpu().numpy()
-        return SvdBatchOut(n=self.n, u_re=cv(self.u_re), u_im=cv(self.u_im),
-                           v_re=cv(self.v_re), v_im=cv(self.v_im),
-                           smax=cv(self.smax), smin=cv(self.smin),
-                           shift=cv(self.shift))
+        return SvdBatchOut(self.n, *(_to_host(getattr(self, k)) for k in _OUT_NAMES))
 
 
-def _reject_nonfinite(a, what):
-    if not np.isfinite(a).all():
+def _require_finite(values, what):
+    if not np.all(np.isfinite(values)):
         raise ValueError("non-finite value in %s" % what)
 
 
 def pack(matrices):
-    """(n, 2, 2) real or complex matrices -> aligned padded Batch2x2, values
-    copied bit-exactly; non-finite entries rejected (layout.py:138-165)."""
+    """(n, 2, 2) real or complex matrices into an aligned padded batch,
+    values copied bit-exactly, non-finite entries rejected
+    (layout.py:138-165)."""
     a = np.asarray(matrices)
     if a.ndim != 3 or a.shape[1:] != (2, 2):
         raise ValueError("expected shape (n, 2, 2), got %r" % (a.shape,))
     n = a.shape[0]
-    n_hat = padded_len(n)
-    cplx = np.iscomplexobj(a)
-    if cplx:
+    if np.iscomplexobj(a):
         a = a.astype(np.complex128, copy=False)
-        _reject_nonfinite(a.real, "matrix real parts")
-        _reject_nonfinite(a.imag, "matrix imaginary parts")
+        _require_finite(a.real, "matrix real parts")
+        _require_finite(a.imag, "matrix imaginary parts")
+        components = (a.real, a.imag)
     else:
         a = a.astype(np.float64, copy=False)
-        _reject_nonfinite(a, "matrix entries")
-    re = aligned_zeros(4, n_hat)
-    im = aligned_zeros(4, n_hat) if cplx else None
-    for t, (i, j) in enumerate(_ENTRY_ORDER):
-        if cplx:
-            re[t, :n] = a[:, i, j].real
-            im[t, :n] = a[:, i, j].imag
-        else:
-            re[t, :n] = a[:, i, j]
-    return Batch2x2(n=n, re=re, im=im)
+        _require_finite(a, "matrix entries")
+        components = (a,)
+    blocks = []
+    for comp in components:
+        block = aligned_zeros(4, padded_len(n))
+        # (n, 2, 2) -> (4, n) in column-major entry order
+        block[:, :n] = comp.transpose(2, 1, 0).reshape(4, n)
+        blocks.append(block)
+    return Batch2x2(n, blocks[0], blocks[1] if len(blocks) > 1 else None)
 
 
 def from_trains(re, im=None, n=None):
-    """Batch from train-ordered (4, m) arrays, copied into aligned padded
-    trains; non-finite genuine lanes rejected (layout.py:168-189)."""
-    re = np.asarray(re, dtype=np.float64)
-    if re.ndim != 2 or re.shape[0] != 4:
-        raise ValueError("expected (4, n) trains, got %r" % (re.shape,))
-    m = re.shape[1] if n is None else int(n)
-    _reject_nonfinite(re[:, :m], "matrix entries")
-    out_re = aligned_zeros(4, padded_len(m))
-    out_re[:, :m] = re[:, :m]
-    out_im = None
+    """A batch from train-ordered (4, m) arrays (the first n lanes, default
+    all), copied into aligned padded blocks; non-finite lanes rejected
+    (layout.py:168-189)."""
+    src = [np.asarray(re, dtype=np.float64)]
+    if src[0].ndim != 2 or src[0].shape[0] != 4:
+        raise ValueError("expected (4, n) trains, got %r" % (src[0].shape,))
     if im is not None:
-        im = np.asarray(im, dtype=np.float64)
-        if im.shape != re.shape:
+        src.append(np.asarray(im, dtype=np.float64))
+        if src[1].shape != src[0].shape:
             raise ValueError("re/im train shapes differ")
-        _reject_nonfinite(im[:, :m], "matrix imaginary parts")
-        out_im = aligned_zeros(4, padded_len(m))
-        out_im[:, :m] = im[:, :m]
-    return Batch2x2(n=m, re=out_re, im=out_im)
+    m = src[0].shape[1] if n is None else int(n)
+    what = ("matrix entries", "matrix imaginary parts")
+    blocks = []
+    for k, s in enumerate(src):
+        _require_finite(s[:, :m], what[k])
+        block = aligned_zeros(4, padded_len(m))
+        np.copyto(block[:, :m], s[:, :m])
+        blocks.append(block)
+    return Batch2x2(m, blocks[0], blocks[1] if len(blocks) > 1 else None)
 
 
-def _matrices(re, im, n):
-    """(n, 2, 2) matrices from (4, >=n) trains."""
-    if im is None:
-        m = np.empty((n, 2, 2), dtype=np.float64)
-    else:
-        m = np.empty((n, 2, 2), dtype=np.complex128)
-    for t, (i, j) in enumerate(_ENTRY_ORDER):
+def _as_matrices(re, im, n):
+    """(n, 2, 2) matrices from the first n lanes of (4, >= n) blocks (parts
+    assigned separately: re + 1j * im would not keep signed zeros)."""
+    out = np.empty((n, 2, 2), dtype=np.float64 if im is None else np.complex128)
+    # out[k, i, j] <- train 2 j + i (column-major entry order)
+    for t, (i, j) in enumerate(ENTRIES):
         if im is None:
-            m[:, i, j] = re[t, :n]
+            out[:, i, j] = re[t, :n]
         else:
-            m[:, i, j].real = re[t, :n]
-            m[:, i, j].imag = im[t, :n]
-    return m
+            out[:, i, j].real = re[t, :n]
+            out[:, i, j].imag = im[t, :n]
+    return out
 
 
 def unpack(out):
-    """Per-matrix records of the n genuine lanes (layout.py:206-224)."""
+    """Per-matrix results of the n genuine lanes (layout.py:206-224)."""
     out = out.cpu()
-    u = _matrices(out.u_re, out.u_im, out.n)
-    v = _matrices(out.v_re, out.v_im, out.n)
-    return [MatrixSvd(u=u[k], v=v[k], smax=float(out.smax[k]),
-                      smin=float(out.smin[k]), shift=float(out.shift[k]))
-            for k in range(out.n)]
+    u = _as_matrices(out.u_re, out.u_im, out.n)
+    v = _as_matrices(out.v_re, out.v_im, out.n)
+    smax, smin, shift = (np.asarray(x)[:out.n].tolist() for x in (out.smax, out.smin, out.shift))
+    return [MatrixSvd(u[k], v[k], smax[k], smin[k], shift[k]) for k in range(out.n)]
 
 
 def unpack_inputs(batch):
-    """(n, 2, 2) array of the genuine input matrices (layout.py:227-238)."""
+    """The genuine input matrices as an (n, 2, 2) array (layout.py:227-238)."""
     batch = batch.cpu()
-    return _matrices(batch.re, batch.im, batch.n)
+    return _as_matrices(batch.re, batch.im, batch.n)

@@ -322,7 +322,9 @@ def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
     bw = pcie_bandwidth(local)
     bound_s = max(n * nin * 8 / (bw["h2d"] * 1e9), n * nout * 8 / (bw["d2h"] * 1e9))
     bound_s = max_over_ranks(bound_s, world)
-    return {"value": n_all / t, "unit": UNIT, "lanes_per_step": n_all,
+    # library default chunk (b2s_host.cu): one streaming kernel + one fix-up per chunk
+    launches = steps * 2 * -(-n // (1 << 22))
+    return {"value": n_all / t, "unit": UNIT, "lanes_per_step": n_all, "gpu_launches": launches,
             "h2d_bytes_per_step": n_all * nin * 8, "d2h_bytes_per_step": n_all * nout * 8,
             "ms_per_step": t * 1e3, "path": "run_batch_into -> b2s_svd2_%s_host (pinned)"
             % cfg["field"],
@@ -425,6 +427,11 @@ def main():
     if not args.no_e2e:
         line["e2e"] = run_e2e(args.config, world, rank, local,
                               max(1, min(args.steps, 5)), 1, args.e2e_lanes)
+        line["gpu_launches"] += line["e2e"]["gpu_launches"]
+    # per timed region: streaming kernel + fix-up per step (and per e2e chunk)
+    line["gpu_launches_detail"] = {"real": res["launches"],
+                                   "complex": line.get("complex") and 2 * args.steps,
+                                   "e2e": line.get("e2e", {}).get("gpu_launches")}
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, done = cpu_sample_rate(args.config)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",

@@ -148,10 +148,38 @@ def barrier(world):
     b()
 
 
+def cpu_model():
+    """The host CPU's model string (lscpu / /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def repo_native_libs():
+    """Shared objects of this repository mapped into this process (the
+    driver checks the reference arm never maps the engine's libb2s.so)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                parts = line.split()
+                if len(parts) >= 6 and parts[-1].endswith(".so") and REPO in parts[-1]:
+                    libs.add(os.path.relpath(parts[-1], REPO))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def cpu_sample_rate(config, budget_s=12.0, sample=1 << 22, threads=None):
-    """Oracle throughput on host cores over a bounded sample of the workload."""
+    """Oracle throughput on host cores over a bounded sample of the workload:
+    the first `sample` lanes of the config, repeated for ~budget_s."""
     import oracle
-    from paper_2005_07403_b200 import synth
+    from paper_2005_07403_b200 import synth   # NumPy generator; loads no native engine code
     threads = threads or os.cpu_count() or 1
     re, im = synth.generate(config, SEED, 0, sample)
     oracle.svd2(re[:, :4096], None if im is None else im[:, :4096], threads=threads)
@@ -163,6 +191,21 @@ def cpu_sample_rate(config, budget_s=12.0, sample=1 << 22, threads=None):
         if el >= budget_s:
             break
     return done / el, threads, done
+
+
+def cpu_baseline_record(config, budget_s=12.0, sample=1 << 22, t1_budget_s=3.0, t1_sample=1 << 18):
+    """the CPU port on all host threads (the value)
+    and on one thread, with the core count and the CPU model."""
+    v, cores, done = cpu_sample_rate(config, budget_s, sample)
+    v1, _, done1 = cpu_sample_rate(config, t1_budget_s, t1_sample, threads=1)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            "value_1thread": v1, "cpu_model": cpu_model(),
+            "sample_lanes": done, "sample_lanes_1thread": done1,
+            "sample": "first 2^%d lanes of config %d, repeated for ~%.0f s (%d lanes in total), "
+                      "through oracle/svd2_oracle.c (C port of lanesvd svd2_lanes + backscale "
+                      "'none', bit-identical outputs) on %d threads; 1-thread rate on the first "
+                      "2^%d lanes" % (sample.bit_length() - 1, config, budget_s, done, cores,
+                                      t1_sample.bit_length() - 1)}
 
 
 def run_device(config, world, rank, local, steps, warmup, with_quality=True):
@@ -348,12 +391,16 @@ def roofline(res, config, hbm, how):
 
 
 def main_reference(args, world, rank):
+    """The reference arm: the CPU port of the reference path (the reference
+    itself is Python + numba and cannot run on the GPU box), timed on all
+    host threads over a bounded sample of the same workload.  Rank 0 only;
+    no GPU work and no engine code (`native_libs` lists what was mapped)."""
     if rank != 0:
         return 0
     import oracle
-    from paper_2005_07403_b200 import synth
+    from paper_2005_07403_b200 import synth   # NumPy generator only
     config = args.config
-    sample = 1 << 22
+    sample = args.ref_sample
     re, im = synth.generate(config, SEED, 0, sample)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -363,18 +410,25 @@ def main_reference(args, world, rank):
         oracle.svd2(re, im, threads=threads)
     el = time.perf_counter() - t0
     v = sample * args.steps / el
+    v1, _, done1 = cpu_sample_rate(config, 3.0, min(sample, 1 << 18), threads=1)
+    cfg = workload_config(config, world)
+    cfg["timed_sample"] = "first %d lanes of the %d-lane workload per step" % (sample, cfg["n"])
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(config, world),
+            "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": "first 2^22 lanes of config %d per step "
+                             "value_1thread": v1, "cpu_model": cpu_model(),
+                             "sample_lanes": sample * args.steps,
+                             "sample_lanes_1thread": done1,
+                             "sample": "first %d lanes of config %d per step "
                                        "(oracle/svd2_oracle.c, C port of lanesvd "
-                                       "svd2_lanes; reference is Python, not "
-                                       "installable on the GPU box)" % config},
+                                       "svd2_lanes; the reference is Python + numba, not "
+                                       "installable on the GPU box)" % (sample, config)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "native_libs": repo_native_libs()}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -400,6 +454,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-lanes", type=int, default=1 << 27)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22,
+                    help="lanes per step of the reference arm's bounded sample")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":
@@ -433,11 +489,7 @@ def main():
                                    "complex": line.get("complex") and 2 * args.steps,
                                    "e2e": line.get("e2e", {}).get("gpu_launches")}
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, done = cpu_sample_rate(args.config)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": "%d lanes of config %d (repeated 2^22-lane "
-                                          "prefix, ~12 s) through oracle/svd2_oracle.c "
-                                          "on %d threads" % (done, args.config, cores)}
+        line["cpu_baseline"] = cpu_baseline_record(args.config)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -6,8 +6,9 @@ power-of-two prescaling, URV reduction to a non-negative triangle, the
 closed-form triangle SVD and the U/V assembly run fused in one kernel per
 field, one matrix per thread, with results bit-identical to the reference.
 
-Compute happens only in ``_native/libb2s.so`` (C ABI: ``include/b2s.h``);
-without it this import fails -- there is no CPU path.
+Compute happens only in ``_native/libb2s.so`` (C ABI: ``include/b2s.h``),
+mapped by the first compute call, which raises if it is not built -- there
+is no CPU path.  Importing the package loads no native code.
 """
 
 from ._lib import LIB_PATH, assert_device_fp_env

@@ -1,7 +1,11 @@
 """ctypes binding of the native engine ``_native/libb2s.so`` (include/b2s.h).
 
-The CUDA library is the only compute path: if it is missing this module
-raises at import, there is no CPU fallback.  Build it with
+The CUDA library is the only compute path.  It is mapped on first use
+(``_lib.lib``), not at import, so that processes which only need the
+package's host-side helpers -- the layout types, the NumPy input generator
+of the CPU baseline -- never load it; the first compute call raises
+``NativeLibraryMissing`` if it is not built.  There is no CPU fallback.
+Build it with
 ``python -c "import __graft_entry__ as g; g.build()"`` (or
 ``python paper_2005_07403_b200/build.py``).
 """
@@ -76,7 +80,25 @@ def _load():
     return L
 
 
-lib = _load()
+_loaded = None
+_load_lock = threading.Lock()
+
+
+def __getattr__(name):
+    # PEP 562: `_lib.lib` maps libb2s.so the first time it is touched.
+    global _loaded
+    if name != "lib":
+        raise AttributeError(name)
+    with _load_lock:
+        if _loaded is None:
+            _loaded = _load()
+            globals()["lib"] = _loaded
+    return _loaded
+
+
+def loaded():
+    """True once libb2s.so has been mapped into this process."""
+    return _loaded is not None
 
 
 def ptr_array(ptrs):

@@ -18,7 +18,7 @@ def test_reference_arm_json_line():
     for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
         env.pop(k, None)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                        "--steps", "1", "--warmup", "0"],
+                        "--steps", "1", "--warmup", "0", "--ref-sample", str(1 << 18)],
                        capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -29,9 +29,25 @@ def test_reference_arm_json_line():
     assert line["config"]["n"] == 1 << 30 and line["config"]["field"] == "real"
     cb = line["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert cb["value_1thread"] > 0 and cb["sample_lanes"] == 1 << 18
+    assert "cpu_model" in cb
+    # the reference arm maps no engine code (it used to load libb2s.so)
+    assert not any("libb2s" in x for x in line["native_libs"]), line["native_libs"]
+    assert "timed_sample" in line["config"]
     e2e = line["e2e"]
     assert e2e["value"] == line["value"] and e2e["unit"] == line["unit"]
     assert e2e["h2d_bytes_per_step"] == 0 and e2e["d2h_bytes_per_step"] == 0
+
+
+def test_package_import_maps_no_native_code():
+    code = ("import paper_2005_07403_b200 as b, paper_2005_07403_b200.synth as s, bench;"
+            "from paper_2005_07403_b200 import _lib;"
+            "s.generate(3, 1, 0, 64);"
+            "assert not _lib.loaded();"
+            "assert not any('libb2s' in x for x in bench.repo_native_libs())")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
 
 
 def test_roofline_object():

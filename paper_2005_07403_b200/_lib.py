@@ -84,16 +84,22 @@ _loaded = None
 _load_lock = threading.Lock()
 
 
-def __getattr__(name):
-    # PEP 562: `_lib.lib` maps libb2s.so the first time it is touched.
+def get():
+    """The mapped library (maps it on first call)."""
     global _loaded
-    if name != "lib":
-        raise AttributeError(name)
     with _load_lock:
         if _loaded is None:
             _loaded = _load()
             globals()["lib"] = _loaded
     return _loaded
+
+
+def __getattr__(name):
+    # PEP 562: `_lib.lib` maps libb2s.so the first time it is touched from
+    # outside; code in this module calls get() (module globals bypass this).
+    if name != "lib":
+        raise AttributeError(name)
+    return get()
 
 
 def loaded():
@@ -111,7 +117,7 @@ def check(rc, what):
     """Map a C-ABI return code onto the reference's exception classes."""
     if rc == 0:
         return
-    msg = "%s: %s" % (what, lib.b2s_last_error().decode(errors="replace"))
+    msg = "%s: %s" % (what, get().b2s_last_error().decode(errors="replace"))
     if rc > 0:
         raise ValueError(msg)
     raise RuntimeError(msg)
@@ -127,5 +133,5 @@ def assert_device_fp_env(device):
     with _env_lock:
         if device in _env_checked:
             return
-        check(lib.b2s_check_fp_env(int(device)), "device FP environment")
+        check(get().b2s_check_fp_env(int(device)), "device FP environment")
         _env_checked.add(device)

@@ -490,6 +490,9 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
   count_hard(A.q, nh);
 }
 
+#if B2S_DIAGNOSTICS
+// Tools-only builds (`build.py --out PATH -DB2S_DIAGNOSTICS=1`); the
+// product library exports exactly the functions include/b2s.h declares.
 // Diagnostic: stream 4 trains through the TMA ring unchanged (tests the
 // ring protocol in isolation; `spin` adds per-lane busy work so warps drift
 // apart).
@@ -564,6 +567,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_traffic_bulk(const RealArgs A) {
   }
   if (tid == 0) tma::bulk_wait<0>();
 }
+#endif  // B2S_DIAGNOSTICS
 
 // Exact fix-up of the marked hard lanes.  Each warp scans 32 mask words
 // (1024 lanes) at a time and appends their set bits to its shared-memory
@@ -1106,6 +1110,7 @@ long long b2s_hard_lane_count(int device) {
   return out;
 }
 
+#if B2S_DIAGNOSTICS
 int b2s_traffic_bulk(int64_t n, const double* const a[4], double* const out[11], void* stream) {
   RealArgs A{};
   A.n = n;
@@ -1131,6 +1136,7 @@ int b2s_ring_probe(int64_t n, const double* const a[4], double* const out[11], i
   B2S_CUDA(cudaGetLastError());
   return 0;
 }
+#endif  // B2S_DIAGNOSTICS
 
 int b2s_check_fp_env(int device) {
   int prev = 0;

@@ -220,13 +220,38 @@ def _declared_symbols():
     return sorted(set(re.findall(r"\b(b2s_[a-z0-9_]+)\s*\(", text)))
 
 
+def _exported_symbols(path):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True,
+                         text=True, check=True).stdout
+    return sorted({ln.split()[-1] for ln in out.splitlines()
+                   if ln.split() and ln.split()[-1].startswith("b2s_")})
+
+
 def test_header_and_library_agree():
+    """Both directions: every function include/b2s.h declares is exported,
+    and the library exports no b2s_ symbol the header does not declare
+    (diagnostic probes live only in the tools build, -DB2S_DIAGNOSTICS)."""
     declared = _declared_symbols()
     assert set(declared) == set(_lib.SYMBOLS)
     raw = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared:
         assert hasattr(raw, name), name
+    assert _exported_symbols(_lib.LIB_PATH) == declared
     assert _lib.lib.b2s_version() >= 100
+
+
+def test_lazy_library_maps_on_first_error_check():
+    """_lib.check() is the first native call of many paths (an argument
+    error before any other call): it must map the library itself."""
+    import subprocess
+    import sys
+    code = ("from paper_2005_07403_b200 import _lib\n"
+            "try:\n    _lib.check(3, 'x')\nexcept ValueError:\n    pass\n"
+            "assert _lib.loaded()\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       cwd=REPO, timeout=300)
+    assert r.returncode == 0, r.stderr
 
 
 def test_library_is_built_for_sm100a():

@@ -3,7 +3,9 @@ read through the TMA ring, 11 written with streaming stores, no math)."""
 import ctypes, os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2005_07403_b200 import _lib
-L = ctypes.CDLL(_lib.LIB_PATH)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _diag
+L = _diag.load()
 L.b2s_ring_probe.argtypes = [ctypes.c_int64, _lib._PA, _lib._PA, ctypes.c_int, ctypes.c_void_p]
 n = 1 << 28
 a = torch.randn(4, n, dtype=torch.float64, device="cuda")

@@ -7,7 +7,9 @@ import ctypes, json, os, sys, time, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2005_07403_b200 import _lib
 import bench
-L = ctypes.CDLL(_lib.LIB_PATH)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _diag
+L = _diag.load()
 L.b2s_ring_probe.argtypes = [ctypes.c_int64, _lib._PA, _lib._PA, ctypes.c_int, ctypes.c_void_p]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 30
 a = torch.ones(4, n, dtype=torch.float64, device="cuda")

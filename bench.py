@@ -138,6 +138,41 @@ def dist_init():
     return world, rank, local
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one per
+    GPU) through torch.distributed.run on 127.0.0.1 and relay rank 0's line.
+    Refuses (exit 2) when fewer than N GPUs are visible -- never times one
+    GPU under an N-GPU label.  B2S_DIST_BACKEND=gloo lets ranks share GPUs
+    (a plumbing check, not a scaling number)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n and os.environ.get("B2S_DIST_BACKEND") != "gloo":
+        print("bench.py: --gpus %d needs %d visible GPUs, found %d" % (n, n, have),
+              file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def rank_devices(local):
+    """(rank, local device ordinal, PCI bus id) of every rank, in rank order."""
+    import torch
+    from paper_2005_07403_b200.dist import gather
+    props = torch.cuda.get_device_properties(local)
+    bus = "%04x:%02x:%02x" % (getattr(props, "pci_domain_id", 0), getattr(props, "pci_bus_id", 0),
+                              getattr(props, "pci_device_id", 0))
+    return gather({"device": local, "pci": bus, "uuid": str(getattr(props, "uuid", ""))})
+
+
 def max_over_ranks(x, world):
     from paper_2005_07403_b200.dist import max_over_ranks as m
     return m(x)
@@ -457,9 +492,14 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 22,
                     help="lanes per step of the reference arm's bounded sample")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return launch_ranks(args.gpus)
     world, rank, local = dist_init()
     if args.impl == "reference":
         return main_reference(args, world, rank)
+    if world != args.gpus:
+        print("bench.py: --gpus %d but %d ranks are running" % (args.gpus, world), file=sys.stderr)
+        return 2
     hbm, how = peaks()
     res = run_device(args.config, world, rank, local, args.steps, args.warmup)
     value = res["n_total"] * args.steps / (res["total_ms"] * 1e-3)
@@ -470,7 +510,7 @@ def main():
             "data": "synthetic", "config": workload_config(args.config, world),
             "roofline": roofline(res, args.config, hbm, how),
             "gpu_launches": res["launches"], "clocks": res["clocks"],
-            "quality": res["quality"]}
+            "quality": res["quality"], "devices": rank_devices(local)}
     if not args.no_complex and args.config == 3:
         cres = run_device(4, world, rank, local, args.steps, args.warmup)
         line["complex"] = {

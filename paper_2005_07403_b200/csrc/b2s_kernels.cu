@@ -178,13 +178,12 @@ __device__ __forceinline__ void redo_cplx(const CplxArgs& A, int64_t i) {
 // Record this warp's hard lanes: one ballot word per 32 consecutive lanes.
 // Lane 0 of the warp always holds the lowest (32-aligned) index.
 // Returns the number of hard lanes in the word (meaningful on lane 0).
-// `members` must name every lane of the warp that holds a lane of this
-// 32-lane word: the full mask inside the TMA tile loops (which also forces
-// warp 0 to reconverge after thread 0's producer work), the active mask in
-// the grid-stride and tail loops.
-__device__ __forceinline__ unsigned mark_hard(const HardQueue& q, bool hard, int64_t i,
-                                              unsigned members = 0xFFFFFFFFu) {
-  const unsigned m = __ballot_sync(members, hard);
+// Every caller reaches it with all 32 lanes of the warp (the loops are
+// warp-uniform and out-of-range lanes pass hard = false), so the ballot
+// uses the full mask -- it also forces warp 0 to reconverge after thread
+// 0's producer work in the TMA kernels.
+__device__ __forceinline__ unsigned mark_hard(const HardQueue& q, bool hard, int64_t i) {
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, hard);
   if ((threadIdx.x & 31) == 0) q.mask[i >> 5] = m;
   return (unsigned)__popc(m);
 }
@@ -200,24 +199,32 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   unsigned long long nh = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-  if (i >= A.n) return;
-  double nx[4];
-  load_real_cs(A, i, nx);
-  for (; i < A.n; i += stride) {
+  // The loop is warp-uniform (lane 0 holds the warp's lowest index): every
+  // lane of a warp iterates while any of its lanes is in range, so the
+  // hard-lane ballot always runs with the full, converged mask.
+  const int64_t lane = threadIdx.x & 31;
+  if (i - lane >= A.n) return;
+  double nx[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < A.n) load_real_cs(A, i, nx);
+  for (; i - lane < A.n; i += stride) {
+    const bool in = i < A.n;
     double a[4] = {nx[0], nx[1], nx[2], nx[3]};
     const int64_t j = i + stride;
     if (j < A.n) load_real_cs(A, j, nx);
     RealOut o;
-    if (States) {
-      LaneStates s;
-      svd2_real_x<Sine, true>(a, o, &s);
-      store_real<Mode>(A, i, o);
-      store_states<false>(A.st, i, s);
-    } else {
-      const bool hard = svd2_real_f<Sine, false>(a, o);
-      store_real<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
-      nh += mark_hard(A.q, hard, i, __activemask());
+    bool hard = false;
+    if (in) {
+      if (States) {
+        LaneStates s;
+        svd2_real_x<Sine, true>(a, o, &s);
+        store_real<Mode>(A, i, o);
+        store_states<false>(A.st, i, s);
+      } else {
+        hard = svd2_real_f<Sine, false>(a, o);
+        store_real<Mode>(A, i, o);    // full sectors; hard lanes are rewritten by the fix-up
+      }
     }
+    if (!States) nh += mark_hard(A.q, hard, i);
   }
   count_hard(A.q, nh);
 }
@@ -227,25 +234,30 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   unsigned long long nh = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-  if (i >= A.n) return;
-  double nr[4], ni[4];
-  load_cplx_cs(A, i, nr, ni);
-  for (; i < A.n; i += stride) {
+  const int64_t lane = threadIdx.x & 31;     // warp-uniform loop, as k_svd2_real
+  if (i - lane >= A.n) return;
+  double nr[4] = {0.0, 0.0, 0.0, 0.0}, ni[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < A.n) load_cplx_cs(A, i, nr, ni);
+  for (; i - lane < A.n; i += stride) {
+    const bool in = i < A.n;
     double ar[4] = {nr[0], nr[1], nr[2], nr[3]};
     double ai[4] = {ni[0], ni[1], ni[2], ni[3]};
     const int64_t j = i + stride;
     if (j < A.n) load_cplx_cs(A, j, nr, ni);
     CplxOut o;
-    if (States) {
-      LaneStates s;
-      svd2_complex_x<Sine, true>(ar, ai, o, &s);
-      store_cplx<Mode>(A, i, o);
-      store_states<true>(A.st, i, s);
-    } else {
-      const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
-      store_cplx<Mode>(A, i, o);      // full sectors; hard lanes are rewritten by the fix-up
-      nh += mark_hard(A.q, hard, i, __activemask());
+    bool hard = false;
+    if (in) {
+      if (States) {
+        LaneStates s;
+        svd2_complex_x<Sine, true>(ar, ai, o, &s);
+        store_cplx<Mode>(A, i, o);
+        store_states<true>(A.st, i, s);
+      } else {
+        hard = svd2_complex_f<Sine, false>(ar, ai, o);
+        store_cplx<Mode>(A, i, o);    // full sectors; hard lanes are rewritten by the fix-up
+      }
     }
+    if (!States) nh += mark_hard(A.q, hard, i);
   }
   count_hard(A.q, nh);
 }
@@ -301,31 +313,31 @@ __device__ __forceinline__ void consumed(const double (&v)[4]) {
 // the warp that brings it to kWarps -- the last reader -- resets it and
 // issues the refill of that stage with the CTA's tile kStages ahead.  No
 // warp ever waits for another except on data, and no thread polls.
-template <int NT>
+template <int NT, int LANES = kBlock, int STAGES = kStages>
 struct TmaRing {
-  static constexpr uint32_t kTileBytes = kBlock * sizeof(double);
-  static constexpr size_t kBuf = (size_t)kStages * NT * kBlock * sizeof(double);
-  static constexpr size_t kSmem = kBuf + kStages * (sizeof(uint64_t) + sizeof(int));
-  double* buf;      // [kStages][NT][kBlock]
-  uint64_t* full;   // [kStages]
-  int* readers;     // [kStages]
+  static constexpr uint32_t kTileBytes = LANES * sizeof(double);
+  static constexpr size_t kBuf = (size_t)STAGES * NT * LANES * sizeof(double);
+  static constexpr size_t kSmem = kBuf + STAGES * (sizeof(uint64_t) + sizeof(int));
+  double* buf;      // [STAGES][NT][LANES]
+  uint64_t* full;   // [STAGES]
+  int* readers;     // [STAGES]
   const double* const* src;
   int64_t mine;
   int64_t tstride;    // elements between consecutive tiles of one source
 
-  __device__ __forceinline__ double* stage(int s, int t) { return buf + ((size_t)s * NT + t) * kBlock; }
+  __device__ __forceinline__ double* stage(int s, int t) { return buf + ((size_t)s * NT + t) * LANES; }
   __device__ __forceinline__ int64_t tile(int64_t j) const { return blockIdx.x + j * gridDim.x; }
 
   __device__ __forceinline__ void init(char* smem, const double* const* src_, int64_t mine_,
-                                      int64_t tstride_ = kBlock) {
+                                      int64_t tstride_ = LANES) {
     buf = reinterpret_cast<double*>(smem);
     full = reinterpret_cast<uint64_t*>(smem + kBuf);
-    readers = reinterpret_cast<int*>(full + kStages);
+    readers = reinterpret_cast<int*>(full + STAGES);
     src = src_;
     mine = mine_;
     tstride = tstride_;
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kStages; s++) {
+      for (int s = 0; s < STAGES; s++) {
         tma::mbar_init(&full[s], 1);
         readers[s] = 0;
       }
@@ -333,7 +345,7 @@ struct TmaRing {
     }
     __syncthreads();
     if (threadIdx.x == 0)
-      for (int64_t j = 0; j < kStages && j < mine; j++) issue((int)j, tile(j));
+      for (int64_t j = 0; j < STAGES && j < mine; j++) issue((int)j, tile(j));
   }
 
   __device__ __forceinline__ void issue(int s, int64_t t) {
@@ -344,20 +356,20 @@ struct TmaRing {
   }
 
   __device__ __forceinline__ void wait_full(int64_t j) {
-    tma::mbar_wait(&full[(int)(j % kStages)], (uint32_t)((j / kStages) & 1));
+    tma::mbar_wait(&full[(int)(j % STAGES)], (uint32_t)((j / STAGES) & 1));
   }
 
   __device__ __forceinline__ void release(int64_t j) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
-      const int s = (int)(j % kStages);
+      const int s = (int)(j % STAGES);
       __threadfence_block();                               // release this warp's reads
-      if (atomicAdd(&readers[s], 1) == kWarps - 1) {
+      if (atomicAdd(&readers[s], 1) == (LANES / 32) - 1) {
         __threadfence_block();                             // acquire the other warps' reads
         readers[s] = 0;
-        if (j + kStages < mine) {
+        if (j + STAGES < mine) {
           tma::fence_proxy_async();
-          issue(s, tile(j + kStages));
+          issue(s, tile(j + STAGES));
         }
       }
     }
@@ -422,13 +434,16 @@ __global__ void __launch_bounds__(kBlock, B2S_REAL_MINB) k_svd2_real_tma(const R
   }
   if (B2S_TMA_TAIL_REAL && blockIdx.x == 0) {
     const int64_t i = tiles * kBlock + tid;
-    if (i < A.n) {
-      double a[4];
-      load_real(A, i, a);
-      RealOut o;
-      const bool hard = svd2_real_f<Sine, false>(a, o);
-      store_real<Mode>(A, i, o);
-      nh += mark_hard(A.q, hard, i, __activemask());
+    if (i - (tid & 31) < A.n) {             // warp-uniform: any lane of the warp in range
+      bool hard = false;
+      if (i < A.n) {
+        double a[4];
+        load_real(A, i, a);
+        RealOut o;
+        hard = svd2_real_f<Sine, false>(a, o);
+        store_real<Mode>(A, i, o);
+      }
+      nh += mark_hard(A.q, hard, i);
     }
   }
   count_hard(A.q, nh);
@@ -478,16 +493,190 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
   }
   if (B2S_TMA_TAIL_CPLX && blockIdx.x == 0) {
     const int64_t i = tiles * kBlock + tid;
-    if (i < A.n) {
-      double ar[4], ai[4];
-      load_cplx(A, i, ar, ai);
-      CplxOut o;
-      const bool hard = svd2_complex_f<Sine, false>(ar, ai, o);
-      store_cplx<Mode>(A, i, o);
-      nh += mark_hard(A.q, hard, i, __activemask());
+    if (i - (tid & 31) < A.n) {             // warp-uniform: any lane of the warp in range
+      bool hard = false;
+      if (i < A.n) {
+        double ar[4], ai[4];
+        load_cplx(A, i, ar, ai);
+        CplxOut o;
+        hard = svd2_complex_f<Sine, false>(ar, ai, o);
+        store_cplx<Mode>(A, i, o);
+      }
+      nh += mark_hard(A.q, hard, i);
     }
   }
   count_hard(A.q, nh);
+}
+
+// ---------------------------------------------------------------------------
+// K2s -- tile-sorted complex streaming kernel (`k_svd2_cplx_sort`).
+//
+// On BASELINE config 4, 10 % of lanes are "wide" (components spanning more
+// than kWideSpread binades) and need the exponent-normalised divisions; in
+// lane order 97 % of warps hold one, so almost every warp paid for them.
+// Here each CTA sorts its tile of LT lanes so the wide lanes fill as few
+// warps as possible (about one of LT / 32), and the outputs go through a
+// shared-memory staging tile written back with one bulk (TMA) store per
+// output train -- whole 2 KiB / 1 KiB rows, so regrouped lanes never split a
+// DRAM sector between writers (the reason the register-store variants of
+// this idea lost).
+//
+// Per tile k (stage s of a TmaRing with B2S_SORT_STAGES stages):
+//   1. every thread classifies its home lane, ballots, lane 0 stores the
+//      warp's wide mask;                                     bar 1
+//   2. every thread computes its home lane's slot (wide lanes first, from a
+//      rotating warp so the wide warp moves across SM sub-partitions) and
+//      writes perm[slot] = lane;                             bar 2
+//   3. warp 0 issues the bulk stores of tile k-1 (staged before bar 1);
+//      thread t gathers lane perm[t]'s inputs, releases the stage, runs the
+//      wide or narrow pipeline (warp-uniform), waits until tile k-1's store
+//      has read the staging tile (mbarrier ofree), stages its 19 outputs and
+//      its hard bit.
+// ---------------------------------------------------------------------------
+#ifndef B2S_CPLX_SORT
+#define B2S_CPLX_SORT 0
+#endif
+#ifndef B2S_SORT_STAGES
+#define B2S_SORT_STAGES 2
+#endif
+#ifndef B2S_SORT_MINB
+#define B2S_SORT_MINB (1536 / (B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 256) < 6 ? 1536 / (B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 256) : 6)
+#endif
+constexpr int kOutCplx = 19;
+
+template <int LT>
+struct SortLayout {
+  using Ring = TmaRing<8, LT, B2S_SORT_STAGES>;
+  static constexpr size_t kRing = (Ring::kSmem + 127) / 128 * 128;
+  static constexpr size_t kOut = (size_t)kOutCplx * LT * sizeof(double);
+  static constexpr size_t kSmem = kRing + kOut + 2 * sizeof(uint64_t) + 2 * (LT / 32) * sizeof(unsigned) +
+                                  LT * sizeof(unsigned short);
+};
+
+__device__ __forceinline__ void bar_named(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Output train t of a complex launch: ur[0..3], ui[0..3], vr[0..3], vi[0..3],
+// smax, smin, shift (the staging tile's row order).
+__device__ __forceinline__ double* cplx_out_train(const CplxArgs& A, int t) {
+  if (t < 4) return A.ur[t];
+  if (t < 8) return A.ui[t - 4];
+  if (t < 12) return A.vr[t - 8];
+  if (t < 16) return A.vi[t - 12];
+  return t == 16 ? A.smax : t == 17 ? A.smin : A.shift;
+}
+
+template <int Mode, bool Sine, int LT>
+__global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const CplxArgs A) {
+  extern __shared__ __align__(128) char smem[];
+  using L = SortLayout<LT>;
+  constexpr int W = LT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* ob = reinterpret_cast<double*>(smem + L::kRing);                 // [19][LT]
+  uint64_t* ofree = reinterpret_cast<uint64_t*>(smem + L::kRing + L::kOut);
+  unsigned* masks = reinterpret_cast<unsigned*>(ofree + 2);               // [W] wide ballots
+  unsigned* hbits = masks + W;                                             // [W] hard bits (tile order)
+  unsigned short* perm = reinterpret_cast<unsigned short*>(hbits + W);     // [LT]
+  const double* src[8];
+  #pragma unroll
+  for (int t = 0; t < 4; t++) { src[t] = A.ar[t]; src[4 + t] = A.ai[t]; }
+  if (tid == 0) tma::mbar_init(ofree, 1);
+  if (tid < W) hbits[tid] = 0;
+  unsigned long long nh = 0;
+  const int64_t tiles = A.n / LT;
+  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  typename L::Ring R;
+  R.init(smem, src, mine, LT);               // fences the barrier inits, __syncthreads
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t k = 0; k < mine; k++) {
+    const int s = (int)(k % B2S_SORT_STAGES);
+    R.wait_full(k);
+    const double* st = R.stage(s, 0);
+    bool w;
+    {
+      double p[8];
+      #pragma unroll
+      for (int t = 0; t < 8; t++) p[t] = st[t * LT + tid];
+      w = wide_lane<8>(p);
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, w);
+    if (lane == 0) masks[warp] = m;
+    bar_named(1, LT);
+    // tile k-1's hard bits (staged in tile order) -> the launch's mask
+    if (k > 0 && tid < W) {
+      const unsigned hb = hbits[tid];
+      A.q.mask[((R.tile(k - 1) * LT) >> 5) + tid] = hb;
+      hbits[tid] = 0;
+      nh += (unsigned)__popc(hb);
+    }
+    int wt = 0, pw = 0;
+    #pragma unroll
+    for (int j = 0; j < W; j++) {
+      const int c = __popc(masks[j]);
+      wt += c;
+      pw += j < warp ? c : 0;
+    }
+    const int pn = warp * 32 - pw;
+    const int r = w ? pw + __popc(m & lt_mask) : wt + pn + __popc(~m & lt_mask);
+    const int rot = (int)((blockIdx.x + (unsigned)k) % W) * 32;
+    perm[(rot + r) & (LT - 1)] = (unsigned short)tid;
+    bar_named(2, LT);
+    if (k > 0 && warp == 0 && lane < kOutCplx) {
+      tma::bulk_store(cplx_out_train(A, lane) + R.tile(k - 1) * LT, ob + lane * LT, LT * sizeof(double));
+      tma::bulk_commit();
+    }
+    const int sl = perm[tid];
+    double ar[4], ai[4];
+    #pragma unroll
+    for (int t = 0; t < 4; t++) { ar[t] = st[t * LT + sl]; ai[t] = st[(4 + t) * LT + sl]; }
+    consumed(ar);
+    consumed(ai);
+    R.release(k);
+    // slot tid holds a wide lane iff it lies in [rot, rot + wt) (mod LT)
+    const bool wide_warp = __any_sync(0xFFFFFFFFu, ((tid - rot) & (LT - 1)) < wt);
+    CplxOut o;
+    bool hard;
+    if (wide_warp)
+      hard = svd2_complex_f<Sine, false, true>(ar, ai, o);
+    else
+      hard = svd2_complex_f<Sine, false, false, true>(ar, ai, o);
+    backscale_lane<Mode>(o.smax, o.smin, o.shift);
+    if (k > 0) {
+      if (warp == 0) {
+        if (lane < kOutCplx) tma::bulk_wait_read<0>();
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(ofree);
+      }
+      tma::mbar_wait(ofree, (uint32_t)((k - 1) & 1));
+    }
+    #pragma unroll
+    for (int t = 0; t < 4; t++) {
+      ob[t * LT + sl] = o.ur[t];
+      ob[(4 + t) * LT + sl] = o.ui[t];
+      ob[(8 + t) * LT + sl] = o.vr[t];
+      ob[(12 + t) * LT + sl] = o.vi[t];
+    }
+    ob[16 * LT + sl] = o.smax;
+    ob[17 * LT + sl] = o.smin;
+    ob[18 * LT + sl] = o.shift;
+    if (hard) atomicOr(&hbits[sl >> 5], 1u << (sl & 31));
+    tma::fence_proxy_async();                 // staged writes -> the bulk stores
+  }
+  bar_named(1, LT);
+  if (mine > 0) {
+    if (tid < W) {
+      const unsigned hb = hbits[tid];
+      A.q.mask[((R.tile(mine - 1) * LT) >> 5) + tid] = hb;
+      nh += (unsigned)__popc(hb);
+    }
+    if (warp == 0 && lane < kOutCplx) {
+      tma::bulk_store(cplx_out_train(A, lane) + R.tile(mine - 1) * LT, ob + lane * LT, LT * sizeof(double));
+      tma::bulk_commit();
+      tma::bulk_wait<0>();
+    }
+  }
+  if (nh) atomicAdd(A.q.cnt, nh);
 }
 
 #if B2S_DIAGNOSTICS
@@ -875,7 +1064,30 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
-    if (!States && (A.aos || tma_ok_cplx(A))) {
+    if (B2S_CPLX_SORT > 0 && !States && !A.aos && tma_ok_cplx(A) && !getenv_flag("B2S_NO_SORT")) {
+      constexpr int LT = B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 128;
+      auto k = k_svd2_cplx_sort<Mode, Sine, LT>;
+      const size_t sm = SortLayout<LT>::kSmem;
+      B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LT, sm);
+      const int64_t tiles = A.n / LT;
+      int64_t g = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+      if (tiles < g) g = tiles;
+      if (g > 0) k<<<(int)g, LT, sm, s>>>(A);
+      const int64_t head = tiles * LT;
+      if (head < A.n) {                           // sub-tile tail: one CTA of the LDG kernel
+        CplxArgs T = A;
+        T.n = A.n - head;
+        for (int t = 0; t < 4; t++) { T.ur[t] += head; T.ui[t] += head; T.vr[t] += head; T.vi[t] += head; }
+        for (int t = 0; t < 4; t++) { T.ar[t] += head; T.ai[t] += head; }
+        T.smax += head; T.smin += head; T.shift += head;
+        T.q.mask += head >> 5;
+        k_svd2_complex<Mode, Sine, false><<<1, kBlock, 0, s>>>(T);
+      }
+    } else if (!States && (A.aos || tma_ok_cplx(A))) {
       auto k = A.aos ? k_svd2_cplx_tma<Mode, Sine, true> : k_svd2_cplx_tma<Mode, Sine, false>;
       const size_t sm = TmaRing<8>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

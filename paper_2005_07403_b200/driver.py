@@ -144,6 +144,20 @@ def _host_trains_ok(batch):
     return True
 
 
+def _check_host_out(out, n_hat):
+    """Caller-owned host outputs: float64, C-contiguous, the batch's shape
+    (the C-ABI writes through raw pointers)."""
+    for name, arr in out.trains().items():
+        want = (n_hat,) if name in ("smax", "smin", "shift") else (4, n_hat)
+        if not isinstance(arr, np.ndarray) or arr.dtype != np.float64:
+            raise ValueError("output %s must be a float64 NumPy array" % name)
+        if tuple(arr.shape) != want:
+            raise ValueError("output %s must have shape %r, got %r"
+                             % (name, want, tuple(arr.shape)))
+        if not arr.flags.c_contiguous or not arr.flags.writeable:
+            raise ValueError("output %s must be C-contiguous and writeable" % name)
+
+
 def run_batch(batch, cfg, sine_form=False, dump_states_to=None):
     """Decompose a whole batch (driver.py:149-190) on the GPU(s).
 
@@ -198,6 +212,7 @@ def run_batch_into(batch, out, cfg, sine_form=False):
                                 _device_out_dict(out, 0, n_hat), mode, flags)
             torch.cuda.synchronize(device)
             return time.perf_counter() - t0
+    _check_host_out(out, n_hat)
     if not _host_trains_ok(batch):
         batch = Batch2x2(n=batch.n, re=np.ascontiguousarray(batch.re, dtype=np.float64),
                          im=None if batch.im is None else

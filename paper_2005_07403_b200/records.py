@@ -112,12 +112,13 @@ def run_records(records, n, field, backscale_mode="none", sine_form=False,
     if device is None:
         device = records.device if is_device_array(records) else \
             torch.device("cuda", torch.cuda.current_device())
-    rec = records if is_device_array(records) else torch.from_numpy(
-        np.ascontiguousarray(records, dtype=np.float64)).to(device)
+    device = torch.device(device)
+    rec = records.to(device=device, dtype=torch.float64) if is_device_array(records) \
+        else torch.from_numpy(np.ascontiguousarray(records, dtype=np.float64)).to(device)
     rec = rec.reshape(-1).contiguous()
     if rec.numel() < -(-n // LANE_WIDTH) * vecs * LANE_WIDTH:
         raise ValueError("records hold fewer than n matrices")
-    _lib.assert_device_fp_env(torch.device(device).index or 0)
+    _lib.assert_device_fp_env(device.index or 0)
     cplx = field == "complex"
     out = SvdBatchOut.empty(n, cplx, device=device)
     rows = lambda a: _lib.ptr_array([a[t].data_ptr() for t in range(4)])
@@ -127,6 +128,12 @@ def run_records(records, n, field, backscale_mode="none", sine_form=False,
     flags = _lib.FLAG_SINE_FORM if sine_form else 0
     mode = _lib.BACKSCALE[backscale_mode]
     n_hat = out.n_hat          # whole records: padding lanes decompose as zero matrices
+    with torch.cuda.device(device):
+        _launch_records(cplx, n_hat, rec, out, u, v, rows, mode, flags, stream)
+    return out
+
+
+def _launch_records(cplx, n_hat, rec, out, u, v, rows, mode, flags, stream):
     if not cplx:
         rc = _lib.lib.b2s_svd2_real_records(n_hat, rec.data_ptr(), u, v,
                                             out.smax.data_ptr(), out.smin.data_ptr(),
@@ -139,4 +146,3 @@ def run_records(records, n, field, backscale_mode="none", sine_form=False,
                                                out.smax.data_ptr(), out.smin.data_ptr(),
                                                out.shift.data_ptr(), mode, flags, stream)
         _lib.check(rc, "b2s_svd2_complex_records")
-    return out

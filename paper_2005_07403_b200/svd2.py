@@ -73,16 +73,62 @@ def _addr(t):
     return t.data_ptr()
 
 
+def check_device_trains(trains, n, device, what):
+    """Every train a float64 CUDA vector on ``device`` with at least ``n``
+    unit-stride elements -- the C-ABI reads and writes raw pointers, so a
+    float32, strided, short or foreign-device tensor would be an
+    out-of-bounds access, not an error, without this check."""
+    import torch
+    for k, t in enumerate(trains):
+        name = "%s[%d]" % (what, k)
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError("%s must be a CUDA tensor" % name)
+        if t.dtype != torch.float64:
+            raise ValueError("%s must be float64, got %s" % (name, t.dtype))
+        if t.dim() != 1 or t.shape[0] < n:
+            raise ValueError("%s must be a vector of >= %d lanes, got shape %s"
+                             % (name, n, tuple(t.shape)))
+        if n > 1 and t.stride(0) != 1:
+            raise ValueError("%s must have unit stride" % name)
+        if t.device != device:
+            raise ValueError("%s is on %s, expected %s" % (name, t.device, device))
+
+
 def launch_device(n, in_re, in_im, out, mode, flags=0, states=None,
                   stream=None):
     """Run the device C-ABI on CUDA tensors.
 
     in_re/in_im: sequences of 4 device trains (in_im None for real);
     out: dict with u_re, u_im, v_re, v_im (sequences of 4 trains) and smax,
-    smin, shift trains; states: sequence of state trains or None.  Launches
-    asynchronously on ``stream`` (default: torch's current stream)."""
-    if stream is None:
-        stream = _stream_of(in_re[0])
+    smin, shift trains; states: sequence of state trains or None.  Every
+    train is validated (float64, unit stride, >= n lanes, one device).
+    Launches asynchronously on ``stream`` (default: torch's current stream
+    of the trains' device), with that device current."""
+    import torch
+    n = int(n)
+    device = in_re[0].device if isinstance(in_re[0], torch.Tensor) else None
+    cplx = in_im is not None
+    if (out.get("u_im") is not None) != cplx or (out.get("v_im") is not None) != cplx:
+        raise ValueError("output trains do not match the field")
+    groups = [("in_re", in_re), ("u_re", out["u_re"]), ("v_re", out["v_re"]),
+              ("smax/smin/shift", [out["smax"], out["smin"], out["shift"]])]
+    if cplx:
+        groups += [("in_im", in_im), ("u_im", out["u_im"]), ("v_im", out["v_im"])]
+    if states is not None:
+        groups.append(("states", states))
+    want = {"smax/smin/shift": 3,
+            "states": len(STATE_NAMES_COMPLEX if cplx else STATE_NAMES_REAL)}
+    for what, trains in groups:
+        if len(trains) != want.get(what, 4):
+            raise ValueError("%s: expected %d trains, got %d"
+                             % (what, want.get(what, 4), len(trains)))
+        check_device_trains(trains, n, device, what)
+    with torch.cuda.device(device):
+        _launch(n, in_re, in_im, out, mode, flags, states,
+                _stream_of(in_re[0]) if stream is None else stream)
+
+
+def _launch(n, in_re, in_im, out, mode, flags, states, stream):
     a, _k1 = _lib.ptr_array([_addr(x) for x in in_re])
     u, _k2 = _lib.ptr_array([_addr(x) for x in out["u_re"]])
     v, _k3 = _lib.ptr_array([_addr(x) for x in out["v_re"]])
@@ -108,7 +154,7 @@ def launch_device(n, in_re, in_im, out, mode, flags=0, states=None,
 def _to_device(x, device):
     import torch
     if is_device_array(x):
-        return x.contiguous()
+        return x.to(device=device, dtype=torch.float64).contiguous()
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(device)
 
 
@@ -126,12 +172,13 @@ def svd2_lanes(parts, sine_form=False, with_states=False, device=None):
     if device is None:
         device = parts[0].device if not host else torch.device(
             "cuda", torch.cuda.current_device())
+    device = torch.device(device)
     dev_parts = [_to_device(p, device) for p in parts]
     n = int(dev_parts[0].shape[0])
     for p in dev_parts:
         if p.shape != (n,):
             raise ValueError("component trains must be equal-length vectors")
-    _lib.assert_device_fp_env(torch.device(device).index or 0)
+    _lib.assert_device_fp_env(device.index or 0)
     cplx = len(parts) == 8
     in_re = dev_parts[0::2] if cplx else dev_parts
     in_im = dev_parts[1::2] if cplx else None
@@ -166,14 +213,17 @@ def backscale(smax_scaled, smin_scaled, shift, mode="safe"):
     host = not is_device_array(smax_scaled)
     device = (smax_scaled.device if not host
               else torch.device("cuda", torch.cuda.current_device()))
-    ins = [_to_device(np.atleast_1d(x) if host else x, device)
+    ins = [_to_device(np.atleast_1d(x) if host else x, device).reshape(-1)
            for x in (smax_scaled, smin_scaled, shift)]
     n = int(ins[0].numel())
+    if any(int(x.numel()) != n for x in ins):
+        raise ValueError("smax, smin and shift must have the same length")
     outs = [torch.empty(n, dtype=torch.float64, device=device)
             for _ in range(3)]
-    rc = _lib.lib.b2s_backscale(n, *[_addr(x) for x in ins],
-                                _lib.BACKSCALE[mode],
-                                *[_addr(x) for x in outs], _stream_of(ins[0]))
+    with torch.cuda.device(device):
+        rc = _lib.lib.b2s_backscale(n, *[_addr(x) for x in ins],
+                                    _lib.BACKSCALE[mode],
+                                    *[_addr(x) for x in outs], _stream_of(ins[0]))
     _lib.check(rc, "b2s_backscale")
     if host:
         return tuple(o.cpu().numpy() for o in outs)

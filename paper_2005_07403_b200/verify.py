@@ -69,12 +69,18 @@ def _run(batch, out, lane_values):
     vr, k5 = P(v_re)
     vi, k6 = P(v_im)
     lp = [l.data_ptr() for l in lanes] if lanes else [None, None, None]
-    rc = _lib.lib.b2s_metrics(n, ar, ai if cplx else None, ur, ui if cplx else None, vr,
+    with torch.cuda.device(device):
+        rc = _metrics_call(n, ar, ai, ur, ui, vr, vi, sv, partial, blocks, lp, cplx, device)
+    _lib.check(rc, "b2s_metrics")
+    return partial.cpu().numpy(), lanes
+
+
+def _metrics_call(n, ar, ai, ur, ui, vr, vi, sv, partial, blocks, lp, cplx, device):
+    import torch
+    return _lib.lib.b2s_metrics(n, ar, ai if cplx else None, ur, ui if cplx else None, vr,
                               vi if cplx else None, sv[0].data_ptr(), sv[1].data_ptr(),
                               sv[2].data_ptr(), partial.data_ptr(), blocks, *lp,
                               torch.cuda.current_stream(device).cuda_stream)
-    _lib.check(rc, "b2s_metrics")
-    return partial.cpu().numpy(), lanes
 
 
 def fold_partials(p):

@@ -68,3 +68,16 @@ def test_workload_configs():
         c = bench.workload_config(config, 1)
         assert c["field"] == field and c["n"] == n and c["workload"].startswith("config%d" % config)
         assert "model" not in c
+
+
+def test_gpus_flag_refuses_when_gpus_are_missing():
+    """`bench.py --gpus 2` outside torchrun launches two ranks itself; with
+    fewer visible GPUs it refuses instead of timing one GPU as two."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "B2S_DIST_BACKEND"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 2 and "needs 2 visible GPUs" in r.stderr, r.stderr
+    assert r.stdout.strip() == ""

@@ -296,3 +296,40 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+# ---------------------------------------------------------------------------
+# Caller-owned buffers are validated before their raw pointers reach the ABI
+# ---------------------------------------------------------------------------
+
+def _host_batch_and_out(n=16, cplx=False):
+    from paper_2005_07403_b200 import SvdBatchOut
+    rng = np.random.default_rng(1)
+    re = rng.standard_normal((4, n))
+    im = rng.standard_normal((4, n)) if cplx else None
+    return b2s.from_trains(re, im), SvdBatchOut.empty(n, cplx)
+
+
+@pytest.mark.parametrize("bad", ["f32", "short", "strided", "readonly", "list"])
+def test_run_batch_into_rejects_bad_host_outputs(bad):
+    batch, out = _host_batch_and_out()
+    if bad == "f32":
+        out.u_re = out.u_re.astype(np.float32)
+    elif bad == "short":
+        out.smax = out.smax[:8]
+    elif bad == "strided":
+        out.v_re = np.zeros((4, 2 * batch.n_hat))[:, ::2]
+    elif bad == "readonly":
+        out.shift.flags.writeable = False
+    else:
+        out.smin = list(out.smin)
+    with pytest.raises(ValueError):
+        b2s.run_batch_into(batch, out, b2s.RunConfig())
+
+
+def test_device_train_check_rejects_host_tensors():
+    import torch
+    from paper_2005_07403_b200.svd2 import check_device_trains
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        check_device_trains([torch.zeros(8, dtype=torch.float64)], 8,
+                            torch.device("cpu"), "in_re")

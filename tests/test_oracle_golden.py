@@ -205,3 +205,18 @@ def test_oracle_states_invariants():
     assert (np.abs(rt) >= np.abs(lt)).all()
     assert (out.smax >= out.smin).all() and (out.smin >= 0).all()
     assert np.isfinite(st).all()
+
+
+def test_train_checksum_numpy_and_torch_agree():
+    """The position-keyed checksums of the full-size golden file: the NumPy
+    form (reference side) and the torch form (device side) are one function."""
+    import torch
+    from helpers import train_checksum_np, train_checksum_torch
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(10_000) * 1e300
+    x[::7] = -0.0
+    for lane0 in (0, 12345, (1 << 30) - 10_000):
+        assert train_checksum_np(x, lane0) == train_checksum_torch(torch.from_numpy(x), lane0)
+    y = x.copy()
+    y[5000] = np.nextafter(y[5000], np.inf)
+    assert train_checksum_np(y, 0) != train_checksum_np(x, 0)

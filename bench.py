@@ -173,6 +173,24 @@ def rank_devices(local):
     return gather({"device": local, "pci": bus, "uuid": str(getattr(props, "uuid", ""))})
 
 
+def sum_over_ranks(x, world):
+    from paper_2005_07403_b200.dist import sum_over_ranks as s
+    return s(x)
+
+
+def reference_quality_counts():
+    """The reference verifier's own over-8-eps lane counts on the golden
+    sample sets (tests/golden/quality_counts.json); the GPU test
+    test_8eps_gate_counts_equal_the_reference checks the engine matches."""
+    p = os.path.join(REPO, "tests", "golden", "quality_counts.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return {k: {"lanes": sum(w[1] for w in v["windows"]),
+                "over_8eps_frobenius": v["over_8eps_frobenius"]} for k, v in d["sets"].items()}
+
+
 def max_over_ranks(x, world):
     from paper_2005_07403_b200.dist import max_over_ranks as m
     return m(x)
@@ -310,6 +328,9 @@ def run_device(config, world, rank, local, steps, warmup, with_quality=True):
                    "kappa_log2": None if f["kappa_inf"] else max_over_ranks(f["kappa"][0], world),
                    "eps": eps, "within_8eps_frobenius": bool(max(rho, dl, et) <= 8 * eps),
                    "within_8eps_2norm": bool(max(rho, d2, e2) <= 8 * eps),
+                   "lanes_over_8eps_frobenius": int(sum_over_ranks(f["over_8eps_frobenius"], world)),
+                   "lanes_over_8eps_2norm": int(sum_over_ranks(f["over_8eps_2norm"], world)),
+                   "reference_counts": reference_quality_counts(),
                    "note": "outputs are bit-identical to the reference, so these are the "
                            "reference algorithm's own error maxima (SURVEY 7.3-1: the literal "
                            "8-eps gate is not met by the reference itself on some complex lanes)",
@@ -354,10 +375,13 @@ def pcie_bandwidth(local, nbytes=1 << 30, reps=4):
     return res
 
 
-def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
-    """Same metric through the host-buffer C-ABI with pinned host trains.
-    Strong-scaled like the device run: max_lanes in total, split over the
-    ranks (bounds the pinned host memory of an 8-GPU run to one copy)."""
+def run_e2e(config, world, rank, local, steps, warmup, max_lanes, pinned=True):
+    """Same metric through the host-buffer C-ABI with host trains: pinned
+    (torch pin_memory) or, with pinned=False, pageable 64-byte-aligned
+    arrays exactly as a lanesvd caller holds them (layout.aligned_zeros,
+    layout.py:42-51), which the library bounces through its own pinned
+    buffers.  Strong-scaled like the device run: max_lanes in total, split
+    over the ranks (bounds the host memory of an 8-GPU run to one copy)."""
     import torch
     import paper_2005_07403_b200 as b2s
     from paper_2005_07403_b200 import synth
@@ -368,7 +392,11 @@ def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
     n = min(hi - lo, max(max_lanes // world, 1 << 20))
     n -= n % 256
     cplx = cfg["field"] == "complex"
-    pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    if pinned:
+        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    else:
+        pin = lambda shape: (b2s.aligned_zeros(*shape) if len(shape) == 2
+                             else b2s.aligned_zeros(1, shape[0])[0])
     # inputs: generated on the device, parked in pinned host memory
     dre, dim = synth.generate_device(config, SEED, lo, n, device=torch.device("cuda", local))
     re = pin((4, n))
@@ -404,25 +432,79 @@ def run_e2e(config, world, rank, local, steps, warmup, max_lanes):
     launches = steps * 2 * -(-n // (1 << 22))
     return {"value": n_all / t, "unit": UNIT, "lanes_per_step": n_all, "gpu_launches": launches,
             "h2d_bytes_per_step": n_all * nin * 8, "d2h_bytes_per_step": n_all * nout * 8,
-            "ms_per_step": t * 1e3, "path": "run_batch_into -> b2s_svd2_%s_host (pinned)"
-            % cfg["field"],
+            "ms_per_step": t * 1e3, "path": "run_batch_into -> b2s_svd2_%s_host (%s)"
+            % (cfg["field"], "pinned" if pinned else
+               "pageable aligned_zeros trains, bounced through the library's pinned buffers"),
+            "config": workload_config(config, world)["workload"],
             "roofline": {"bound": "host link (PCIe)", "h2d_gbs": round(bw["h2d"], 1),
                          "d2h_gbs": round(bw["d2h"], 1), "bound_ms": round(bound_s * 1e3, 2),
                          "frac": round(bound_s / t, 4),
                          "how": "1 GiB pinned copies, both directions at once, per GPU"}}
 
 
-def roofline(res, config, hbm, how):
+def fp64_peak(local=0):
+    """FP64 peak (TFLOP/s, DFMA = 2 flops) of this GPU: measured live with
+    the FP64 probe (tools/csrc/fp64_peak.cu, built by __graft_entry__.build)
+    when it is built, else the committed B200 measurement
+    (profiles/r2_fp64_peak.json).  MEASURED_PEAKS.json has no FP64 figure."""
+    so = os.path.join(REPO, "tools", "_build", "libfp64_peak.so")
+    import torch
+    if os.path.exists(so) and torch.cuda.is_available():
+        try:
+            import ctypes
+            L = ctypes.CDLL(so)
+            L.fp64_peak.argtypes = [ctypes.c_int, ctypes.c_longlong, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_float)]
+            v, ms = ctypes.c_double(), ctypes.c_float()
+            with torch.cuda.device(local):
+                if L.fp64_peak(0, 200000, 8, ctypes.byref(v), ctypes.byref(ms)) == 0:
+                    return round(2 * v.value / 1e12, 3), "measured live (tools/csrc/fp64_peak.cu DFMA probe)"
+        except (OSError, RuntimeError):
+            pass
+    p = os.path.join(REPO, "profiles", "r2_fp64_peak.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["dfma_tflops"]), "profiles/r2_fp64_peak.json (B200 DFMA probe)"
+    return None, "unmeasured"
+
+
+def ncu_record(config):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as fh:
+        return json.load(fh).get(str(config)) or {}
+
+
+def roofline(res, config, hbm, how, fp64=(None, "unmeasured")):
+    """The kernel's two roofline terms (north_star "% of
+    HBM/FP64 roofline"): algorithmic bytes over the measured HBM copy peak
+    and algorithmic FP64 flops over the measured FP64 peak, per launch;
+    `bound` is the binding (larger-fraction) term.  The issued FP64-pipe
+    utilisation (correctly rounded divisions and square roots expand to
+    ~9 FP64 instructions each) comes from the committed ncu capture."""
     field = res["field"]
+    secs = res["avg_kernel_ms"] * 1e-3
     bytes_per_launch = BYTES_PER_SVD[field] * res["n_shard"]
-    achieved = bytes_per_launch / (res["avg_kernel_ms"] * 1e-3) / 1e9
+    achieved = bytes_per_launch / secs / 1e9
     traffic = ncu_traffic(config, res["n_shard"])
-    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-            "unit": "GB/s", "frac": round(achieved / hbm, 4), "peak_source": how,
+    flops = FLOPS_PER_SVD[field] * res["n_shard"]
+    tflops = flops / secs / 1e12
+    peak64, how64 = fp64
+    rec = ncu_record(config)
+    fp = {"algorithmic_tflops": round(tflops, 3), "peak_tflops": peak64,
+          "frac": round(tflops / peak64, 4) if peak64 else None, "peak_source": how64,
+          "algorithmic_flops_per_svd": FLOPS_PER_SVD[field],
+          "issued_fp64_pipe_frac": (round(rec["fp64_pipe_pct"] / 100, 4)
+                                    if "fp64_pipe_pct" in rec else None),
+          "issued_source": rec.get("report")}
+    hbm_frac = achieved / hbm
+    bound = "hbm" if not peak64 or hbm_frac >= tflops / peak64 else "fp64"
+    return {"bound": bound, "achieved": round(achieved, 1), "peak": hbm,
+            "unit": "GB/s", "frac": round(hbm_frac, 4), "peak_source": how,
             "traffic": traffic,
             "algorithmic_bytes_per_launch": bytes_per_launch,
-            "fp64_tflops": round(FLOPS_PER_SVD[field] * res["n_shard"]
-                                 / (res["avg_kernel_ms"] * 1e-3) / 1e12, 3)}
+            "fp64_tflops": round(tflops, 3), "fp64": fp}
 
 
 def main_reference(args, world, rank):
@@ -501,6 +583,7 @@ def main():
         print("bench.py: --gpus %d but %d ranks are running" % (args.gpus, world), file=sys.stderr)
         return 2
     hbm, how = peaks()
+    fp64 = fp64_peak(local)
     res = run_device(args.config, world, rank, local, args.steps, args.warmup)
     value = res["n_total"] * args.steps / (res["total_ms"] * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -508,7 +591,7 @@ def main():
             "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args.config, world),
-            "roofline": roofline(res, args.config, hbm, how),
+            "roofline": roofline(res, args.config, hbm, how, fp64),
             "gpu_launches": res["launches"], "clocks": res["clocks"],
             "quality": res["quality"], "devices": rank_devices(local)}
     if not args.no_complex and args.config == 3:
@@ -517,17 +600,28 @@ def main():
             "value": cres["n_total"] * args.steps / (cres["total_ms"] * 1e-3),
             "unit": UNIT, "ms_per_step": cres["total_ms"] / args.steps,
             "config": workload_config(4, world),
-            "roofline": roofline(cres, 4, hbm, how), "clocks": cres["clocks"],
+            "roofline": roofline(cres, 4, hbm, how, fp64), "clocks": cres["clocks"],
             "quality": cres["quality"]}
         line["gpu_launches"] += cres["launches"]
     if not args.no_e2e:
-        line["e2e"] = run_e2e(args.config, world, rank, local,
-                              max(1, min(args.steps, 5)), 1, args.e2e_lanes)
+        e2e_steps = max(1, min(args.steps, 5))
+        line["e2e"] = run_e2e(args.config, world, rank, local, e2e_steps, 1, args.e2e_lanes)
         line["gpu_launches"] += line["e2e"]["gpu_launches"]
+        # the same call as a drop-in lanesvd caller makes it: pageable trains
+        line["e2e_pageable"] = run_e2e(args.config, world, rank, local, e2e_steps, 1,
+                                       args.e2e_lanes, pinned=False)
+        line["gpu_launches"] += line["e2e_pageable"]["gpu_launches"]
+        if not args.no_complex and args.config == 3:
+            line["complex"]["e2e"] = run_e2e(4, world, rank, local, e2e_steps, 1,
+                                             args.e2e_lanes // 2)
+            line["gpu_launches"] += line["complex"]["e2e"]["gpu_launches"]
     # per timed region: streaming kernel + fix-up per step (and per e2e chunk)
     line["gpu_launches_detail"] = {"real": res["launches"],
                                    "complex": line.get("complex") and 2 * args.steps,
-                                   "e2e": line.get("e2e", {}).get("gpu_launches")}
+                                   "e2e": line.get("e2e", {}).get("gpu_launches"),
+                                   "e2e_pageable": line.get("e2e_pageable", {}).get("gpu_launches"),
+                                   "complex_e2e": (line.get("complex") or {}).get("e2e", {})
+                                   .get("gpu_launches")}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_record(args.config)
     if rank == 0:

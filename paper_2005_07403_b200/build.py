@@ -20,7 +20,7 @@ HEADERS = ["csrc/b2s_lane.cuh", "csrc/b2s_svd2.cuh", "csrc/b2s_fast.cuh", "csrc/
 OUT = os.path.join(HERE, "_native", "libb2s.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",
               "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
-              "-fPIC", "-shared"]
+              "-fPIC,-fopenmp", "-shared", "-lgomp"]
 
 
 def _stale():

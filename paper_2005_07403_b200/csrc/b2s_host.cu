@@ -6,6 +6,17 @@
 // kernel, copy-out of the output trains, round-robin over three streams so
 // the H2D of chunk c+1, the kernel of chunk c and the D2H of chunk c-1
 // overlap.  Device staging buffers are cached per device between calls.
+//
+// Pageable host trains (a lanesvd caller's aligned_zeros arrays,
+// layout.py:42-51) cannot be copied asynchronously: cudaMemcpyAsync from
+// pageable memory is staged synchronously by the driver and the copy /
+// compute / copy overlap collapses.  When any train is pageable the
+// pipeline bounces every chunk through per-stage pinned host buffers
+// instead, filled and drained by the host cores in parallel (OpenMP) while
+// the GPU streams other stages -- no page pinning of the caller's memory.
+#include <omp.h>
+
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -23,7 +34,45 @@ struct DeviceCtx {
   cudaEvent_t done[kStages];
   double* buf[kStages] = {nullptr, nullptr, nullptr};
   size_t buf_bytes = 0;
+  double* hbuf[kStages] = {nullptr, nullptr, nullptr};   // pinned bounce buffers (pageable callers)
+  size_t hbuf_bytes = 0;
 };
+
+static bool pageable(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+static int ensure_host(DeviceCtx& c, size_t bytes) {
+  if (c.hbuf_bytes >= bytes) return 0;
+  for (int s = 0; s < kStages; s++) {
+    if (c.hbuf[s]) cudaFreeHost(c.hbuf[s]);
+    c.hbuf[s] = nullptr;
+  }
+  c.hbuf_bytes = 0;
+  for (int s = 0; s < kStages; s++) B2S_CUDA(cudaMallocHost(&c.hbuf[s], bytes));
+  c.hbuf_bytes = bytes;
+  return 0;
+}
+
+// Parallel copy of `ntr` trains' chunks (host cores; each train split into
+// 1 MiB pieces so every thread has work).
+static void par_copy(int ntr, double* const* dst, const double* const* src, int64_t m) {
+  const int64_t piece = 1 << 17;                     // doubles
+  const int64_t per = (m + piece - 1) / piece;
+  const int64_t total = per * ntr;
+  #pragma omp parallel for schedule(static)
+  for (int64_t w = 0; w < total; w++) {
+    const int t = (int)(w / per);
+    const int64_t lo = (w % per) * piece;
+    const int64_t len = (m - lo) < piece ? (m - lo) : piece;
+    std::memcpy(dst[t] + lo, src[t] + lo, (size_t)len * sizeof(double));
+  }
+}
 
 static DeviceCtx& ctx_for(int dev) {
   static DeviceCtx ctxs[64];
@@ -46,6 +95,66 @@ static int ensure(DeviceCtx& c, size_t bytes) {
     c.buf_bytes = 0;
     for (int s = 0; s < kStages; s++) B2S_CUDA(cudaMalloc(&c.buf[s], bytes));
     c.buf_bytes = bytes;
+  }
+  return 0;
+}
+
+// Chunked pipeline through pinned bounce buffers: chunk k's inputs are
+// copied into stage k % 3's pinned buffer by the host cores, streamed in,
+// decomposed and streamed back into the same stage's pinned buffer; its
+// outputs are copied to the caller when the stage comes round again (or at
+// the end), so host copies of one stage overlap the GPU work of the others.
+template <typename Launch>
+static int bounce_pipeline(DeviceCtx& c, int64_t n, int64_t chunk, int n_in, const double* const* in,
+                           int n_out, double* const* out, Launch launch) {
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  std::vector<const double*> src(n_in > n_out ? n_in : n_out);
+  std::vector<double*> dst(n_in > n_out ? n_in : n_out);
+  auto drain = [&](int64_t k) -> int {                 // chunk k's outputs -> caller
+    const int s = (int)(k % kStages);
+    B2S_CUDA(cudaEventSynchronize(c.done[s]));
+    const int64_t lo = k * chunk;
+    const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
+    for (int t = 0; t < n_out; t++) {
+      src[t] = c.hbuf[s] + (size_t)(n_in + t) * chunk;
+      dst[t] = out[t] + lo;
+    }
+    par_copy(n_out, dst.data(), src.data(), m);
+    return 0;
+  };
+  for (int64_t k = 0; k < nchunks; k++) {
+    const int s = (int)(k % kStages);
+    cudaStream_t st = c.streams[s];
+    if (k >= kStages) {
+      int rc = drain(k - kStages);
+      if (rc) return rc;
+    }
+    const int64_t lo = k * chunk;
+    const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
+    const size_t mb = (size_t)m * sizeof(double);
+    for (int t = 0; t < n_in; t++) {
+      src[t] = in[t] + lo;
+      dst[t] = c.hbuf[s] + (size_t)t * chunk;
+    }
+    par_copy(n_in, dst.data(), src.data(), m);
+    std::vector<const double*> din(n_in);
+    std::vector<double*> dout(n_out);
+    for (int t = 0; t < n_in; t++) {
+      double* d = c.buf[s] + (size_t)t * chunk;
+      B2S_CUDA(cudaMemcpyAsync(d, c.hbuf[s] + (size_t)t * chunk, mb, cudaMemcpyHostToDevice, st));
+      din[t] = d;
+    }
+    for (int t = 0; t < n_out; t++) dout[t] = c.buf[s] + (size_t)(n_in + t) * chunk;
+    int rc = launch(m, din.data(), dout.data(), st);
+    if (rc) return rc;
+    for (int t = 0; t < n_out; t++)
+      B2S_CUDA(cudaMemcpyAsync(c.hbuf[s] + (size_t)(n_in + t) * chunk, dout[t], mb, cudaMemcpyDeviceToHost,
+                               st));
+    B2S_CUDA(cudaEventRecord(c.done[s], st));
+  }
+  for (int64_t k = nchunks > kStages ? nchunks - kStages : 0; k < nchunks; k++) {
+    int rc = drain(k);
+    if (rc) return rc;
   }
   return 0;
 }
@@ -77,6 +186,14 @@ static int pipeline(int64_t n, int device, int64_t chunk, int n_in, const double
   int rc = ensure(c, tbytes * trains);
   if (rc) return rc;
   const int64_t nchunks = (n + chunk - 1) / chunk;
+  bool bounce = false;
+  for (int t = 0; t < n_in; t++) bounce |= pageable(in[t]);
+  for (int t = 0; t < n_out; t++) bounce |= pageable(out[t]);
+  if (bounce) {
+    rc = ensure_host(c, tbytes * trains);
+    if (rc) return rc;
+    return bounce_pipeline(c, n, chunk, n_in, in, n_out, out, launch);
+  }
   for (int64_t k = 0; k < nchunks; k++) {
     const int s = (int)(k % kStages);
     cudaStream_t st = c.streams[s];

@@ -589,6 +589,8 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
   typename L::Ring R;
   R.init(smem, src, mine, LT);               // fences the barrier inits, __syncthreads
   const unsigned lt_mask = (1u << lane) - 1u;
+  // warp 0's lanes 0..18 each own one output train's bulk store
+  double* const my_dst = (warp == 0 && lane < kOutCplx) ? cplx_out_train(A, lane) : nullptr;
   for (int64_t k = 0; k < mine; k++) {
     const int s = (int)(k % B2S_SORT_STAGES);
     R.wait_full(k);
@@ -622,8 +624,8 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
     const int rot = (int)((blockIdx.x + (unsigned)k) % W) * 32;
     perm[(rot + r) & (LT - 1)] = (unsigned short)tid;
     bar_named(2, LT);
-    if (k > 0 && warp == 0 && lane < kOutCplx) {
-      tma::bulk_store(cplx_out_train(A, lane) + R.tile(k - 1) * LT, ob + lane * LT, LT * sizeof(double));
+    if (k > 0 && my_dst) {
+      tma::bulk_store(my_dst + R.tile(k - 1) * LT, ob + lane * LT, LT * sizeof(double));
       tma::bulk_commit();
     }
     const int sl = perm[tid];
@@ -633,6 +635,14 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
     consumed(ar);
     consumed(ai);
     R.release(k);
+    // Warp 0 frees the staging tile as soon as tile k-1's stores have read
+    // it (a few hundred cycles after the issue), long before any warp needs
+    // it again, so the other warps' ofree waits below do not spin.
+    if (k > 0 && warp == 0) {
+      if (my_dst) tma::bulk_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(ofree);
+    }
     // slot tid holds a wide lane iff it lies in [rot, rot + wt) (mod LT)
     const bool wide_warp = __any_sync(0xFFFFFFFFu, ((tid - rot) & (LT - 1)) < wt);
     CplxOut o;
@@ -642,14 +652,7 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
     else
       hard = svd2_complex_f<Sine, false, false, true>(ar, ai, o);
     backscale_lane<Mode>(o.smax, o.smin, o.shift);
-    if (k > 0) {
-      if (warp == 0) {
-        if (lane < kOutCplx) tma::bulk_wait_read<0>();
-        __syncwarp();
-        if (lane == 0) tma::mbar_arrive(ofree);
-      }
-      tma::mbar_wait(ofree, (uint32_t)((k - 1) & 1));
-    }
+    if (k > 0) tma::mbar_wait(ofree, (uint32_t)((k - 1) & 1));
     #pragma unroll
     for (int t = 0; t < 4; t++) {
       ob[t * LT + sl] = o.ur[t];
@@ -670,8 +673,8 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
       A.q.mask[((R.tile(mine - 1) * LT) >> 5) + tid] = hb;
       nh += (unsigned)__popc(hb);
     }
-    if (warp == 0 && lane < kOutCplx) {
-      tma::bulk_store(cplx_out_train(A, lane) + R.tile(mine - 1) * LT, ob + lane * LT, LT * sizeof(double));
+    if (my_dst) {
+      tma::bulk_store(my_dst + R.tile(mine - 1) * LT, ob + lane * LT, LT * sizeof(double));
       tma::bulk_commit();
       tma::bulk_wait<0>();
     }

@@ -164,11 +164,12 @@ __device__ __forceinline__ DD gram_deviation2(CD c11, CD c21, CD c12, CD c22) {
 // Per-block partial: rho, delta, eta (hi, lo), kappa (d, qhi, qlo), kappa
 // infinite flag, excluded-lane count, then the spectral-norm delta2, eta2
 // (hi, lo).
-constexpr int kPartial = 15;
+constexpr int kPartial = 17;
 
 struct Acc {
   double rho_hi, rho_lo, del_hi, del_lo, eta_hi, eta_lo, kd, kq_hi, kq_lo, kinf, bad;
   double d2_hi, d2_lo, e2_hi, e2_lo;
+  double over_f, over_2;     // lanes with max(rho, delta, eta) > 8 eps (Frobenius / 2-norm)
 };
 
 // Lexicographic maximum helpers (NaN in hi propagates, like numpy.max).
@@ -195,11 +196,13 @@ __device__ __forceinline__ void merge(Acc& a, const Acc& b) {
   a.bad += b.bad;
   max_dd(a.d2_hi, a.d2_lo, b.d2_hi, b.d2_lo);
   max_dd(a.e2_hi, a.e2_lo, b.e2_hi, b.e2_lo);
+  a.over_f += b.over_f;
+  a.over_2 += b.over_2;
 }
 
 __device__ __forceinline__ Acc acc_identity() {
   const double ninf = -__longlong_as_double(0x7FF0000000000000ll);
-  return {ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, 0.0, 0.0, ninf, ninf, ninf, ninf};
+  return {ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, ninf, 0.0, 0.0, ninf, ninf, ninf, ninf, 0.0, 0.0};
 }
 
 struct MetricArgs {
@@ -258,6 +261,13 @@ __device__ Acc lane_metrics(const MetricArgs& M, int64_t i) {
   const DD e2 = gram_deviation2(v[0], v[1], v[2], v[3]);
   r.d2_hi = d2.hi; r.d2_lo = d2.lo;
   r.e2_hi = e2.hi; r.e2_lo = e2.lo;
+  // north_star's 8-eps gate per lane (eps = 2^-52), exact on the DD values
+  const double tol = 0x1p-49;
+  auto over = [&](const DD& x) { return x.hi > tol || (x.hi == tol && x.lo > 0.0); };
+  const bool of = over(rho) || over(delta) || over(eta);
+  const bool o2 = over(rho) || over(d2) || over(e2);
+  r.over_f = of ? 1.0 : 0.0;
+  r.over_2 = o2 ? 1.0 : 0.0;
   if (bad || smin == 0.0) {
     r.kinf = 1.0;
   } else {

@@ -16,6 +16,8 @@ components out of the record layout in shared memory
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -39,21 +41,29 @@ def _field(field):
 
 
 def read_records(path, field):
-    """Validated (n_records, vecs, 8) float64 array of a test file."""
+    """Validated (n_records, vecs, 8) float64 array of a test file.
+
+    Raises DataError -- as lanesvd.cli.read_testfile does (cli.py:102-134)
+    -- when the file cannot be opened, holds no data, is not a whole number
+    of records, or contains a NaN or an infinity."""
     vecs = _field(field)
-    record_bytes = vecs * LANE_WIDTH * 8
+    rec_doubles = vecs * LANE_WIDTH
     try:
-        raw = np.fromfile(path, dtype="<f8")
+        size = os.stat(path).st_size
+        data = np.fromfile(path, dtype="<f8") if size else np.empty(0)
     except OSError as exc:
         raise DataError("cannot read %s: %s" % (path, exc))
-    if raw.size == 0:
+    if size == 0:
         raise DataError("%s is empty" % path)
-    if (raw.size * 8) % record_bytes:
-        raise DataError("%s is not a whole number of %d-byte %s records"
-                        % (path, record_bytes, field))
-    if not np.isfinite(raw).all():
-        raise DataError("%s contains non-finite values" % path)
-    return np.ascontiguousarray(raw.astype(np.float64, copy=False)).reshape(-1, vecs, LANE_WIDTH)
+    n_rec, extra = divmod(size, rec_doubles * 8)
+    if extra:
+        raise DataError("%s: %d bytes is not a multiple of the %d-byte %s record"
+                        % (path, size, rec_doubles * 8, field))
+    finite = np.isfinite(data)
+    if not finite.all():
+        raise DataError("%s: non-finite value at element %d"
+                        % (path, int(np.argmin(finite))))
+    return data.astype(np.float64, copy=False).reshape(n_rec, vecs, LANE_WIDTH)
 
 
 def records_to_trains(recs, field):

@@ -21,7 +21,7 @@ from .layout import is_device_array
 
 __all__ = ["Metrics", "metrics", "lane_metrics", "fold_partials"]
 
-_NPART = 15
+_NPART = 17
 
 
 @dataclass
@@ -99,7 +99,8 @@ def fold_partials(p):
     qlo = np.max(p[sel, 8])
     return {"rho": rho, "delta": delta, "eta": eta, "kappa": (dmax, qhi, qlo),
             "kappa_inf": bool(np.max(p[:, 9]) > 0), "excluded": int(np.sum(p[:, 10])),
-            "delta2": dd_max(p[:, 11], p[:, 12]), "eta2": dd_max(p[:, 13], p[:, 14])}
+            "delta2": dd_max(p[:, 11], p[:, 12]), "eta2": dd_max(p[:, 13], p[:, 14]),
+            "over_8eps_frobenius": int(np.sum(p[:, 15])), "over_8eps_2norm": int(np.sum(p[:, 16]))}
 
 
 def metrics(batch, out):

@@ -63,6 +63,22 @@ def test_roofline_object():
     assert bench.roofline(cres, 4, 6454.3, "measured")["algorithmic_bytes_per_launch"] == 216 * (1 << 28)
 
 
+def test_roofline_fp64_term():
+    """Both roofline terms: 70 / 178 algorithmic flops per SVD over the
+    measured FP64 peak, the binding term named, the issued FP64-pipe
+    fraction from the committed ncu capture."""
+    peak, how = bench.fp64_peak()
+    assert peak and 20 < peak < 60, (peak, how)       # B200 DFMA ~37 TFLOP/s
+    res = {"field": "complex", "n_shard": 1 << 28, "avg_kernel_ms": 16.0}
+    rf = bench.roofline(res, 4, 6454.3, "measured", (peak, how))
+    fp = rf["fp64"]
+    assert abs(fp["algorithmic_tflops"] - 178 * (1 << 28) / 0.016 / 1e12) < 1e-3
+    assert abs(fp["frac"] - fp["algorithmic_tflops"] / peak) < 1e-3
+    assert rf["bound"] == "hbm" and 0 < fp["issued_fp64_pipe_frac"] < 1
+    slow = bench.roofline(res, 4, 6454.3, "measured", (0.01, "tiny"))
+    assert slow["bound"] == "fp64"
+
+
 def test_workload_configs():
     for config, field, n in ((3, "real", 1 << 30), (4, "complex", 1 << 28)):
         c = bench.workload_config(config, 1)

@@ -54,8 +54,8 @@ def test_single_equals_chunk_equals_batch_bitwise(field):
         lane = b2s.unpack(chunk)[k]
         assert_bits_equal(np.array([one.smax, one.smin, one.shift]),
                           np.array([lane.smax, lane.smin, lane.shift]), "sigma lane %d" % k)
-        assert_bits_equal(np.ascontiguousarray(one.u), np.ascontiguousarray(lane.u), "u lane %d" % k)
-        assert_bits_equal(np.ascontiguousarray(one.v), np.ascontiguousarray(lane.v), "v lane %d" % k)
+        assert_bits_equal(np.ascontiguousarray(one.u).view(np.float64), np.ascontiguousarray(lane.u).view(np.float64), "u lane %d" % k)
+        assert_bits_equal(np.ascontiguousarray(one.v).view(np.float64), np.ascontiguousarray(lane.v).view(np.float64), "v lane %d" % k)
 
 
 def _outd(out):
@@ -133,3 +133,40 @@ def test_non_current_device_launches_on_the_tensors_device():  # pragma: no cove
     assert got.smax_scaled.device == dev1
     assert_bits_equal(got.smax_scaled.cpu().numpy(), ref.smax, "svd2_lanes smax")
     assert_bits_equal(out.cpu().smax, ref.smax, "run_batch smax")
+
+
+@pytest.mark.parametrize("layout", ["pinned", "pageable", "mixed"])
+def test_host_path_pinned_and_pageable_trains(layout):
+    """The host-buffer C-ABI streams pinned trains directly and bounces
+    pageable ones (a lanesvd caller's aligned_zeros arrays) through its own
+    pinned buffers; every combination gives the oracle's trains, across
+    several pipeline chunks and a ragged last chunk."""
+    n = 3 * 65536 + 1000
+    for config in (2, 4):
+        re, im = synth.generate(config, 12, 0, n)
+        cplx = im is not None
+        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+        page = lambda shape: (b2s.aligned_zeros(*shape) if len(shape) == 2
+                              else b2s.aligned_zeros(1, shape[0])[0])
+        n_hat = b2s.padded_len(n)
+        alloc_in = pin if layout in ("pinned", "mixed") else page
+        alloc_out = pin if layout == "pinned" else page
+        bre = alloc_in((4, n_hat))
+        bre[:] = 0.0
+        bre[:, :n] = re
+        bim = None
+        if cplx:
+            bim = alloc_in((4, n_hat))
+            bim[:] = 0.0
+            bim[:, :n] = im
+        batch = b2s.Batch2x2(n=n, re=bre, im=bim)
+        out = b2s.SvdBatchOut(n=n, u_re=alloc_out((4, n_hat)),
+                              u_im=alloc_out((4, n_hat)) if cplx else None,
+                              v_re=alloc_out((4, n_hat)),
+                              v_im=alloc_out((4, n_hat)) if cplx else None,
+                              smax=alloc_out((n_hat,)), smin=alloc_out((n_hat,)),
+                              shift=alloc_out((n_hat,)))
+        b2s.run_batch_into(batch, out, b2s.RunConfig(field=batch.field, chunk=65536))
+        ref = oracle.svd2(batch.re, batch.im)
+        for name, arr in ref.trains().items():
+            assert_bits_equal(out.trains()[name], arr, "%s %s" % (layout, name))

@@ -71,3 +71,22 @@ def test_tolerance_gate_at_scale():
     eps = 2.0 ** -52
     assert f["rho"][0] <= 8 * eps and f["delta"][0] <= 8 * eps and f["eta"][0] <= 8 * eps
     assert int((rho > 8 * eps).sum()) == 0
+
+
+def test_8eps_gate_counts_equal_the_reference():
+    """Lanes over north_star's 8-eps gate (rho, delta or eta, Frobenius),
+    counted by the GPU verifier on the engine's outputs, equal the counts
+    the reference's own verifier gives on its outputs
+    (tests/golden/quality_counts.json, make_quality_counts.py)."""
+    from paper_2005_07403_b200.verify import _run, fold_partials
+    with open(os.path.join(GOLDEN, "quality_counts.json")) as fh:
+        ref = json.load(fh)
+    dev = torch.device("cuda", 0)
+    for name, rec in ref["sets"].items():
+        total = 0
+        for lo, n in rec["windows"]:
+            re, im = synth.generate_device(rec["config"], ref["seed"], lo, n, device=dev)
+            b = b2s.Batch2x2(n=n, re=re, im=im)
+            out, _ = b2s.run_batch(b, b2s.RunConfig(field=b.field))
+            total += fold_partials(_run(b, out, False)[0])["over_8eps_frobenius"]
+        assert total == rec["over_8eps_frobenius"], (name, total, rec["over_8eps_frobenius"])

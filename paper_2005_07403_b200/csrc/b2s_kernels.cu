@@ -453,6 +453,9 @@ template <int Mode, bool Sine, bool AoS>
 #ifndef B2S_CPLX_MINB
 #define B2S_CPLX_MINB 3
 #endif
+#ifndef B2S_CPLX_STAGES
+#define B2S_CPLX_STAGES kStages
+#endif
 __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const CplxArgs A) {
   extern __shared__ __align__(128) char smem[];
   const double* src[8];
@@ -465,10 +468,10 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
   unsigned long long nh = 0;
   const int64_t tiles = A.n / kBlock;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  TmaRing<8> R;
+  TmaRing<8, kBlock, B2S_CPLX_STAGES> R;
   R.init(smem, src, mine, AoS ? 8 * kBlock : kBlock);
   for (int64_t k = 0; k < mine; k++) {
-    const int s = (int)(k % kStages);
+    const int s = (int)(k % B2S_CPLX_STAGES);
     R.wait_full(k);
     double ar[4], ai[4];
     #pragma unroll
@@ -509,53 +512,55 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
 }
 
 // ---------------------------------------------------------------------------
-// K2s -- tile-sorted complex streaming kernel (`k_svd2_cplx_sort`).
+// K2s -- tile-sorted, warp-specialised complex streaming kernel
+// (`k_svd2_cplx_ws`).
 //
 // On BASELINE config 4, 10 % of lanes are "wide" (components spanning more
 // than kWideSpread binades) and need the exponent-normalised divisions; in
 // lane order 97 % of warps hold one, so almost every warp paid for them.
-// Here each CTA sorts its tile of LT lanes so the wide lanes fill as few
-// warps as possible (about one of LT / 32), and the outputs go through a
-// shared-memory staging tile written back with one bulk (TMA) store per
-// output train -- whole 2 KiB / 1 KiB rows, so regrouped lanes never split a
-// DRAM sector between writers (the reason the register-store variants of
-// this idea lost).
+// Here each tile of LT lanes is sorted so the wide lanes fill as few warps
+// as possible (about one of LT / 32), and the outputs go through a shared-
+// memory staging tile written back with one bulk (TMA) store per output
+// train -- whole rows, so regrouped lanes never split a DRAM sector between
+// writers (why the register-store regroupings of round 1 lost, DESIGN.md
+// section 3).
 //
-// Per tile k (stage s of a TmaRing with B2S_SORT_STAGES stages):
-//   1. every thread classifies its home lane, ballots, lane 0 stores the
-//      warp's wide mask;                                     bar 1
-//   2. every thread computes its home lane's slot (wide lanes first, from a
-//      rotating warp so the wide warp moves across SM sub-partitions) and
-//      writes perm[slot] = lane;                             bar 2
-//   3. warp 0 issues the bulk stores of tile k-1 (staged before bar 1);
-//      thread t gathers lane perm[t]'s inputs, releases the stage, runs the
-//      wide or narrow pipeline (warp-uniform), waits until tile k-1's store
-//      has read the staging tile (mbarrier ofree), stages its 19 outputs and
-//      its hard bit.
+// Warp specialisation keeps the LT / 32 compute warps free of CTA barriers
+// (a barrier-per-tile version of this kernel measured 21 % barrier stalls):
+// one producer warp per CTA
+//   * issues the TMA loads of a kSortStages-deep input ring,
+//   * classifies each landed tile (8 components per lane), computes the
+//     lane permutation (wide lanes first, from a rotating warp so the wide
+//     warp moves across SM sub-partitions) and publishes it (mbarrier plan),
+//   * once every compute warp has staged tile k's outputs (mbarrier ofull),
+//     issues the tile's 19 bulk stores and hard-lane mask words, and frees
+//     the staging tile when the stores have read it (mbarrier oempty).
+// A compute warp waits only on data: the plan of its tile (ready a tile
+// ahead) and, before staging, the read-out of the previous tile -- so warps
+// drift up to one tile apart instead of meeting at a barrier every tile.
 // ---------------------------------------------------------------------------
 #ifndef B2S_CPLX_SORT
 #define B2S_CPLX_SORT 0
 #endif
+#if B2S_CPLX_SORT   // measured and rejected; variant builds only
 #ifndef B2S_SORT_STAGES
-#define B2S_SORT_STAGES 2
+#define B2S_SORT_STAGES 3
 #endif
 #ifndef B2S_SORT_MINB
-#define B2S_SORT_MINB (1536 / (B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 256) < 6 ? 1536 / (B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 256) : 6)
+#define B2S_SORT_MINB 5
 #endif
 constexpr int kOutCplx = 19;
 
 template <int LT>
-struct SortLayout {
-  using Ring = TmaRing<8, LT, B2S_SORT_STAGES>;
-  static constexpr size_t kRing = (Ring::kSmem + 127) / 128 * 128;
+struct WsLayout {
+  static constexpr int S = B2S_SORT_STAGES;
+  static constexpr int W = LT / 32;
+  static constexpr size_t kIn = (size_t)S * 8 * LT * sizeof(double);
   static constexpr size_t kOut = (size_t)kOutCplx * LT * sizeof(double);
-  static constexpr size_t kSmem = kRing + kOut + 2 * sizeof(uint64_t) + 2 * (LT / 32) * sizeof(unsigned) +
-                                  LT * sizeof(unsigned short);
+  static constexpr size_t kBars = (size_t)(3 * S + 2) * sizeof(uint64_t);
+  static constexpr size_t kSmem = kIn + kOut + kBars + S * sizeof(int) + W * sizeof(unsigned) +
+                                  (size_t)S * LT * sizeof(unsigned short);
 };
-
-__device__ __forceinline__ void bar_named(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 
 // Output train t of a complex launch: ur[0..3], ui[0..3], vr[0..3], vi[0..3],
 // smax, smin, shift (the staging tile's row order).
@@ -568,81 +573,135 @@ __device__ __forceinline__ double* cplx_out_train(const CplxArgs& A, int t) {
 }
 
 template <int Mode, bool Sine, int LT>
-__global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const CplxArgs A) {
+__global__ void __launch_bounds__(LT + 32, B2S_SORT_MINB) k_svd2_cplx_ws(const CplxArgs A) {
   extern __shared__ __align__(128) char smem[];
-  using L = SortLayout<LT>;
-  constexpr int W = LT / 32;
+  using L = WsLayout<LT>;
+  constexpr int S = L::S, W = L::W;
+  double* in = reinterpret_cast<double*>(smem);                            // [S][8][LT]
+  double* ob = reinterpret_cast<double*>(smem + L::kIn);                   // [19][LT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kIn + L::kOut);   // [S] TMA landed
+  uint64_t* empty = full + S;                                              // [S] gathered (W arrivals)
+  uint64_t* plan = empty + S;                                              // [S] permutation ready
+  uint64_t* ofull = plan + S;                                              // staged (W arrivals)
+  uint64_t* oempty = ofull + 1;                                            // stores have read ob
+  int* meta = reinterpret_cast<int*>(oempty + 1);                          // [S] wide count | rot << 16
+  unsigned* hbits = reinterpret_cast<unsigned*>(meta + S);                 // [W] hard bits, tile order
+  unsigned short* perm = reinterpret_cast<unsigned short*>(hbits + W);     // [S][LT] slot -> lane
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* ob = reinterpret_cast<double*>(smem + L::kRing);                 // [19][LT]
-  uint64_t* ofree = reinterpret_cast<uint64_t*>(smem + L::kRing + L::kOut);
-  unsigned* masks = reinterpret_cast<unsigned*>(ofree + 2);               // [W] wide ballots
-  unsigned* hbits = masks + W;                                             // [W] hard bits (tile order)
-  unsigned short* perm = reinterpret_cast<unsigned short*>(hbits + W);     // [LT]
-  const double* src[8];
-  #pragma unroll
-  for (int t = 0; t < 4; t++) { src[t] = A.ar[t]; src[4 + t] = A.ai[t]; }
-  if (tid == 0) tma::mbar_init(ofree, 1);
-  if (tid < W) hbits[tid] = 0;
-  unsigned long long nh = 0;
   const int64_t tiles = A.n / LT;
   const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  typename L::Ring R;
-  R.init(smem, src, mine, LT);               // fences the barrier inits, __syncthreads
-  const unsigned lt_mask = (1u << lane) - 1u;
-  // warp 0's lanes 0..18 each own one output train's bulk store
-  double* const my_dst = (warp == 0 && lane < kOutCplx) ? cplx_out_train(A, lane) : nullptr;
-  for (int64_t k = 0; k < mine; k++) {
-    const int s = (int)(k % B2S_SORT_STAGES);
-    R.wait_full(k);
-    const double* st = R.stage(s, 0);
-    bool w;
-    {
-      double p[8];
-      #pragma unroll
-      for (int t = 0; t < 8; t++) p[t] = st[t * LT + tid];
-      w = wide_lane<8>(p);
+  auto tile = [&](int64_t j) { return (int64_t)blockIdx.x + j * gridDim.x; };
+  auto stage = [&](int s) { return in + (size_t)s * 8 * LT; };
+  if (tid == 0) {
+    for (int s = 0; s < S; s++) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], W);
+      tma::mbar_init(&plan[s], 1);
     }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, w);
-    if (lane == 0) masks[warp] = m;
-    bar_named(1, LT);
-    // tile k-1's hard bits (staged in tile order) -> the launch's mask
-    if (k > 0 && tid < W) {
-      const unsigned hb = hbits[tid];
-      A.q.mask[((R.tile(k - 1) * LT) >> 5) + tid] = hb;
-      hbits[tid] = 0;
-      nh += (unsigned)__popc(hb);
-    }
-    int wt = 0, pw = 0;
+    tma::mbar_init(ofull, W);
+    tma::mbar_init(oempty, 1);
+    tma::fence_init();
+  }
+  if (tid < W) hbits[tid] = 0;
+  __syncthreads();
+
+  if (warp == W) {
+    // ------------------------------ producer ------------------------------
+    const double* src[8];
     #pragma unroll
-    for (int j = 0; j < W; j++) {
-      const int c = __popc(masks[j]);
-      wt += c;
-      pw += j < warp ? c : 0;
+    for (int t = 0; t < 4; t++) { src[t] = A.ar[t]; src[4 + t] = A.ai[t]; }
+    double* const my_dst = lane < kOutCplx ? cplx_out_train(A, lane) : nullptr;
+    const uint64_t pol = tma::evict_first_policy();
+    auto load = [&](int s, int64_t j) {
+      tma::mbar_arrive_expect_tx(&full[s], 8 * LT * sizeof(double));
+      #pragma unroll
+      for (int t = 0; t < 8; t++)
+        tma::bulk_load(stage(s) + t * LT, src[t] + tile(j) * LT, LT * sizeof(double), &full[s], pol);
+    };
+    if (lane == 0)
+      for (int64_t j = 0; j < S && j < mine; j++) load((int)j, j);
+    unsigned long long nh = 0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    auto store = [&](int64_t j) {                    // tile j's staged outputs -> HBM
+      tma::mbar_wait_sleep(ofull, (uint32_t)(j & 1));
+      if (lane < W) {
+        const unsigned hb = hbits[lane];
+        A.q.mask[((tile(j) * LT) >> 5) + lane] = hb;
+        hbits[lane] = 0;
+        nh += (unsigned)__popc(hb);
+      }
+      if (my_dst) {
+        tma::bulk_store(my_dst + tile(j) * LT, ob + lane * LT, LT * sizeof(double));
+        tma::bulk_commit();
+        tma::bulk_wait_read<0>();
+      }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(oempty);
+    };
+    for (int64_t j = 0; j < mine; j++) {
+      const int s = (int)(j % S);
+      tma::mbar_wait_sleep(&full[s], (uint32_t)((j / S) & 1));
+      const double* st = stage(s);
+      unsigned m[W];
+      int wt = 0;
+      #pragma unroll
+      for (int q = 0; q < W; q++) {
+        double p[8];
+        #pragma unroll
+        for (int t = 0; t < 8; t++) p[t] = st[t * LT + q * 32 + lane];
+        m[q] = __ballot_sync(0xFFFFFFFFu, wide_lane<8>(p));
+        wt += __popc(m[q]);
+      }
+      const int rot = (int)((blockIdx.x + (unsigned)j) % W);
+      int pw = 0;
+      unsigned short* pm = perm + (size_t)s * LT;
+      #pragma unroll
+      for (int q = 0; q < W; q++) {
+        const bool w = (m[q] >> lane) & 1u;
+        const int pn = q * 32 - pw;                  // narrow lanes before this group
+        const int r = w ? pw + __popc(m[q] & lt_mask) : wt + pn + __popc(~m[q] & lt_mask);
+        pm[(rot * 32 + r) & (LT - 1)] = (unsigned short)(q * 32 + lane);
+        pw += __popc(m[q]);
+      }
+      if (lane == 0) meta[s] = wt | (rot << 16);
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&plan[s]);
+      if (j > 0) {
+        store(j - 1);
+        // refill tile j-1's stage (its lanes were gathered before its outputs were staged)
+        const int ps = (int)((j - 1) % S);
+        if (lane == 0 && j - 1 + S < mine) {
+          tma::mbar_wait_sleep(&empty[ps], (uint32_t)(((j - 1) / S) & 1));
+          load(ps, j - 1 + S);
+        }
+        __syncwarp();
+      }
     }
-    const int pn = warp * 32 - pw;
-    const int r = w ? pw + __popc(m & lt_mask) : wt + pn + __popc(~m & lt_mask);
-    const int rot = (int)((blockIdx.x + (unsigned)k) % W) * 32;
-    perm[(rot + r) & (LT - 1)] = (unsigned short)tid;
-    bar_named(2, LT);
-    if (k > 0 && my_dst) {
-      tma::bulk_store(my_dst + R.tile(k - 1) * LT, ob + lane * LT, LT * sizeof(double));
-      tma::bulk_commit();
+    if (mine > 0) {
+      store(mine - 1);
+      if (my_dst) tma::bulk_wait<0>();
     }
-    const int sl = perm[tid];
+    if (nh) atomicAdd(A.q.cnt, nh);
+    return;
+  }
+
+  // ------------------------------ compute warps ------------------------------
+  for (int64_t k = 0; k < mine; k++) {
+    const int s = (int)(k % S);
+    const uint32_t par = (uint32_t)((k / S) & 1);
+    tma::mbar_wait(&full[s], par);
+    tma::mbar_wait(&plan[s], par);
+    const int mt = meta[s];
+    const int wt = mt & 0xFFFF, rot = (mt >> 16) * 32;
+    const int sl = perm[(size_t)s * LT + tid];
+    const double* st = stage(s);
     double ar[4], ai[4];
     #pragma unroll
     for (int t = 0; t < 4; t++) { ar[t] = st[t * LT + sl]; ai[t] = st[(4 + t) * LT + sl]; }
     consumed(ar);
     consumed(ai);
-    R.release(k);
-    // Warp 0 frees the staging tile as soon as tile k-1's stores have read
-    // it (a few hundred cycles after the issue), long before any warp needs
-    // it again, so the other warps' ofree waits below do not spin.
-    if (k > 0 && warp == 0) {
-      if (my_dst) tma::bulk_wait_read<0>();
-      __syncwarp();
-      if (lane == 0) tma::mbar_arrive(ofree);
-    }
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[s]);
     // slot tid holds a wide lane iff it lies in [rot, rot + wt) (mod LT)
     const bool wide_warp = __any_sync(0xFFFFFFFFu, ((tid - rot) & (LT - 1)) < wt);
     CplxOut o;
@@ -652,7 +711,7 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
     else
       hard = svd2_complex_f<Sine, false, false, true>(ar, ai, o);
     backscale_lane<Mode>(o.smax, o.smin, o.shift);
-    if (k > 0) tma::mbar_wait(ofree, (uint32_t)((k - 1) & 1));
+    if (k > 0) tma::mbar_wait(oempty, (uint32_t)((k - 1) & 1));
     #pragma unroll
     for (int t = 0; t < 4; t++) {
       ob[t * LT + sl] = o.ur[t];
@@ -665,22 +724,12 @@ __global__ void __launch_bounds__(LT, B2S_SORT_MINB) k_svd2_cplx_sort(const Cplx
     ob[18 * LT + sl] = o.shift;
     if (hard) atomicOr(&hbits[sl >> 5], 1u << (sl & 31));
     tma::fence_proxy_async();                 // staged writes -> the bulk stores
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(ofull);
   }
-  bar_named(1, LT);
-  if (mine > 0) {
-    if (tid < W) {
-      const unsigned hb = hbits[tid];
-      A.q.mask[((R.tile(mine - 1) * LT) >> 5) + tid] = hb;
-      nh += (unsigned)__popc(hb);
-    }
-    if (my_dst) {
-      tma::bulk_store(my_dst + R.tile(mine - 1) * LT, ob + lane * LT, LT * sizeof(double));
-      tma::bulk_commit();
-      tma::bulk_wait<0>();
-    }
-  }
-  if (nh) atomicAdd(A.q.cnt, nh);
 }
+
+#endif  // B2S_CPLX_SORT
 
 #if B2S_DIAGNOSTICS
 // Tools-only builds (`build.py --out PATH -DB2S_DIAGNOSTICS=1`); the
@@ -1067,19 +1116,20 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
-    if (B2S_CPLX_SORT > 0 && !States && !A.aos && tma_ok_cplx(A) && !getenv_flag("B2S_NO_SORT")) {
+#if B2S_CPLX_SORT
+    if (!States && !A.aos && tma_ok_cplx(A) && !getenv_flag("B2S_NO_SORT")) {
       constexpr int LT = B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 128;
-      auto k = k_svd2_cplx_sort<Mode, Sine, LT>;
-      const size_t sm = SortLayout<LT>::kSmem;
+      auto k = k_svd2_cplx_ws<Mode, Sine, LT>;
+      const size_t sm = WsLayout<LT>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       int dev = 0, sms = 148, per_sm = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LT, sm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LT + 32, sm);
       const int64_t tiles = A.n / LT;
       int64_t g = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
       if (tiles < g) g = tiles;
-      if (g > 0) k<<<(int)g, LT, sm, s>>>(A);
+      if (g > 0) k<<<(int)g, LT + 32, sm, s>>>(A);
       const int64_t head = tiles * LT;
       if (head < A.n) {                           // sub-tile tail: one CTA of the LDG kernel
         CplxArgs T = A;
@@ -1090,9 +1140,11 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
         T.q.mask += head >> 5;
         k_svd2_complex<Mode, Sine, false><<<1, kBlock, 0, s>>>(T);
       }
-    } else if (!States && (A.aos || tma_ok_cplx(A))) {
+    } else
+#endif
+    if (!States && (A.aos || tma_ok_cplx(A))) {
       auto k = A.aos ? k_svd2_cplx_tma<Mode, Sine, true> : k_svd2_cplx_tma<Mode, Sine, false>;
-      const size_t sm = TmaRing<8>::kSmem;
+      const size_t sm = TmaRing<8, kBlock, B2S_CPLX_STAGES>::kSmem;
       B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k<<<tma_grid(k, sm, A.n), kBlock, sm, s>>>(A);
       const int64_t head = A.n / kBlock * kBlock;

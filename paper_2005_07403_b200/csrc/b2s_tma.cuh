@@ -65,6 +65,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Blocking wait that parks the thread between polls (suspend-time hint,
+// NANOSLEEP.SYNCS): for waiters that are expected to wait long (a producer
+// warp waiting for a whole tile of compute), so they do not burn issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity), "n"(20000)
+      : "memory");
+}
+
 // Non-blocking probe: true once the phase of the given parity completed.
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;

@@ -42,10 +42,18 @@ extern "C" {
 /* flags */
 #define B2S_FLAG_SINE_FORM 1   /* svd2_lanes(sine_form=True), svd2.py:427-474 */
 #define B2S_FLAG_STATES 2      /* also write the _dump_states trains, driver.py:193-216 */
+#define B2S_FLAG_STATES_FULL 4 /* with B2S_FLAG_STATES: also the rest of svd2_lanes'
+                                  with_states tuple (svd2.py:62-105, 568-569) */
 
 /* Number of state trains written with B2S_FLAG_STATES (driver.py:193-216). */
 #define B2S_STATES_REAL 16
 #define B2S_STATES_COMPLEX 20
+/* ... and with B2S_FLAG_STATES | B2S_FLAG_STATES_FULL: the above, then
+ * TriangleSvd left_sec2, left_cos, right_sec2, right_cos, then
+ * ScaleResult.parts (the scaled component trains, input order: 4 real /
+ * 8 complex re,im-interleaved). */
+#define B2S_STATES_REAL_FULL 24
+#define B2S_STATES_COMPLEX_FULL 32
 
 /* ABI version (major*100 + minor). */
 int b2s_version(void);
@@ -61,7 +69,8 @@ const char *b2s_last_error(void);
  *   a[4]      device pointers to the input trains e11, e21, e12, e22
  *   u[4],v[4] device pointers to the output trains u11, u21, u12, u22 / v..
  *   smax, smin, shift   device pointers, n doubles each
- *   states    NULL, or B2S_STATES_REAL device train pointers (needs
+ *   states    NULL, or B2S_STATES_REAL (B2S_STATES_REAL_FULL with
+ *             B2S_FLAG_STATES_FULL) device train pointers (needs
  *             B2S_FLAG_STATES)
  * Every pointer must be 8-byte aligned (the trains of aligned_zeros / torch
  *            storage are 64-byte aligned, which the kernels exploit).

@@ -24,6 +24,7 @@ LIB_PATH = os.environ.get("B2S_LIBRARY") or os.path.join(_HERE, "_native", "libb
 BACKSCALE = {"none": 0, "safe": 1, "unconditional": 2}
 FLAG_SINE_FORM = 1
 FLAG_STATES = 2
+FLAG_STATES_FULL = 4
 STATES_REAL = 16
 STATES_COMPLEX = 20
 

@@ -46,4 +46,8 @@ inline int grid_for(K kernel, int block, int64_t work_items, int* err) {
   return (int)(need < full ? need : full);
 }
 
+// Argument checks shared by the device and host-buffer entry points
+// (b2s_kernels.cu): batch size, backscale mode, flag bits, states array.
+int check_common(int64_t n, int mode, int flags, double* const* states);
+
 }  // namespace b2s

@@ -228,6 +228,7 @@ int b2s_svd2_real_host(int64_t n, const double* const a[4], double* const u[4], 
                        int64_t chunk) {
   if (!a || !u || !v || !smax || !smin || !shift) return fail(5, "NULL host train");
   if (flags & B2S_FLAG_STATES) return fail(3, "state dumps are device-only (use b2s_svd2_real)");
+  if (int rc = check_common(n, backscale_mode, flags, nullptr)) return rc;    // before any CUDA call
   const double* in[4] = {a[0], a[1], a[2], a[3]};
   double* out[11] = {u[0], u[1], u[2], u[3], v[0], v[1], v[2], v[3], smax, smin, shift};
   for (int t = 0; t < 4; t++) if (!in[t]) return fail(5, "NULL host train");
@@ -246,6 +247,7 @@ int b2s_svd2_complex_host(int64_t n, const double* const a_re[4], const double* 
   if (!a_re || !a_im || !u_re || !u_im || !v_re || !v_im || !smax || !smin || !shift)
     return fail(5, "NULL host train");
   if (flags & B2S_FLAG_STATES) return fail(3, "state dumps are device-only (use b2s_svd2_complex)");
+  if (int rc = check_common(n, backscale_mode, flags, nullptr)) return rc;    // before any CUDA call
   const double* in[8] = {a_re[0], a_re[1], a_re[2], a_re[3], a_im[0], a_im[1], a_im[2], a_im[3]};
   double* out[19] = {u_re[0], u_re[1], u_re[2], u_re[3], u_im[0], u_im[1], u_im[2], u_im[3],
                      v_re[0], v_re[1], v_re[2], v_re[3], v_im[0], v_im[1], v_im[2], v_im[3],

@@ -42,7 +42,8 @@ struct RealArgs {
   double* u[4];
   double* v[4];
   double *smax, *smin, *shift;
-  double* st[B2S_STATES_COMPLEX];
+  double* st[B2S_STATES_COMPLEX_FULL];
+  int full_states;      // B2S_FLAG_STATES_FULL
 };
 
 struct CplxArgs {
@@ -53,7 +54,8 @@ struct CplxArgs {
   const double* ai[4];
   double *ur[4], *ui[4], *vr[4], *vi[4];
   double *smax, *smin, *shift;
-  double* st[B2S_STATES_COMPLEX];
+  double* st[B2S_STATES_COMPLEX_FULL];
+  int full_states;
 };
 
 constexpr int kBlock = 256;
@@ -62,7 +64,7 @@ __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p);
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 
 template <bool Cplx>
-__device__ __forceinline__ void store_states(double* const* st, int64_t i, const LaneStates& s) {
+__device__ __forceinline__ void store_states(double* const* st, int64_t i, const LaneStates& s, bool full) {
   int k = 0;
   st_stream(st[k++] + i, s.shift);
   st_stream(st[k++] + i, s.swap_c);
@@ -80,6 +82,14 @@ __device__ __forceinline__ void store_states(double* const* st, int64_t i, const
   st_stream(st[k++] + i, s.r_tan);
   st_stream(st[k++] + i, s.smax);
   st_stream(st[k++] + i, s.smin);
+  if (full) {
+    st_stream(st[k++] + i, s.l_sec2);
+    st_stream(st[k++] + i, s.l_cos);
+    st_stream(st[k++] + i, s.r_sec2);
+    st_stream(st[k++] + i, s.r_cos);
+    #pragma unroll
+    for (int t = 0; t < (Cplx ? 8 : 4); t++) st_stream(st[k++] + i, s.sp[t]);
+  }
 }
 
 template <int Mode>
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_svd2_real(const RealArgs A) {
         LaneStates s;
         svd2_real_x<Sine, true>(a, o, &s);
         store_real<Mode>(A, i, o);
-        store_states<false>(A.st, i, s);
+        store_states<false>(A.st, i, s, A.full_states != 0);
       } else {
         hard = svd2_real_f<Sine, false>(a, o);
         store_real<Mode>(A, i, o);    // full sectors; hard lanes are rewritten by the fix-up
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
         LaneStates s;
         svd2_complex_x<Sine, true>(ar, ai, o, &s);
         store_cplx<Mode>(A, i, o);
-        store_states<true>(A.st, i, s);
+        store_states<true>(A.st, i, s, A.full_states != 0);
       } else {
         hard = svd2_complex_f<Sine, false>(ar, ai, o);
         store_cplx<Mode>(A, i, o);    // full sectors; hard lanes are rewritten by the fix-up
@@ -1059,7 +1069,7 @@ static int launch_real(RealArgs A, cudaStream_t s) {
     if (A.aos) A.a[0] += lo * 4;                 // 32 doubles per 8 lanes
     else for (int t = 0; t < 4; t++) A.a[t] += lo;
     A.smax += lo; A.smin += lo; A.shift += lo;
-    if (States) for (int k = 0; k < B2S_STATES_REAL; k++) A.st[k] += lo;
+    if (States) for (int k = 0; k < (A.full_states ? B2S_STATES_REAL_FULL : B2S_STATES_REAL); k++) A.st[k] += lo;
     if (!States) {
       int rc = get_queue(W, s, A.n, &A.q);
       if (rc) return rc;
@@ -1110,7 +1120,7 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
     if (A.aos) A.ar[0] += lo * 8;                // 64 doubles per 8 lanes
     else for (int t = 0; t < 4; t++) { A.ar[t] += lo; A.ai[t] += lo; }
     A.smax += lo; A.smin += lo; A.shift += lo;
-    if (States) for (int k = 0; k < B2S_STATES_COMPLEX; k++) A.st[k] += lo;
+    if (States) for (int k = 0; k < (A.full_states ? B2S_STATES_COMPLEX_FULL : B2S_STATES_COMPLEX); k++) A.st[k] += lo;
     if (!States) {
       int rc = get_queue(W, s, A.n, &A.q);
       if (rc) return rc;
@@ -1194,11 +1204,14 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
     return LAUNCH<2, false, false>(A, s);                                                \
   } while (0)
 
-static int check_common(int64_t n, int mode, int flags, double* const* states) {
+int check_common(int64_t n, int mode, int flags, double* const* states) {
   if (n < 0) return fail(1, "negative batch size %lld", (long long)n);
   if (mode < 0 || mode > 2) return fail(2, "backscale_mode must be 0 (none), 1 (safe) or 2 (unconditional), got %d", mode);
-  if (flags & ~(B2S_FLAG_SINE_FORM | B2S_FLAG_STATES)) return fail(3, "unknown flag bits 0x%x", flags);
+  if (flags & ~(B2S_FLAG_SINE_FORM | B2S_FLAG_STATES | B2S_FLAG_STATES_FULL))
+    return fail(3, "unknown flag bits 0x%x", flags);
   if ((flags & B2S_FLAG_STATES) && !states) return fail(4, "B2S_FLAG_STATES needs a states train array");
+  if ((flags & B2S_FLAG_STATES_FULL) && !(flags & B2S_FLAG_STATES))
+    return fail(3, "B2S_FLAG_STATES_FULL needs B2S_FLAG_STATES");
   return 0;
 }
 
@@ -1226,8 +1239,13 @@ int real_entry(int64_t n, const double* const a[4], double* const u[4], double* 
   B2S_CHECK_PTR(smax, "smax"); B2S_CHECK_PTR(smin, "smin"); B2S_CHECK_PTR(shift, "shift");
   A.smax = smax; A.smin = smin; A.shift = shift;
   bool st = flags & B2S_FLAG_STATES;
-  if (st)
-    for (int k = 0; k < B2S_STATES_REAL; k++) { B2S_CHECK_PTR(states[k], "state train"); A.st[k] = states[k]; }
+  if (st) {
+    A.full_states = (flags & B2S_FLAG_STATES_FULL) != 0;
+    for (int k = 0; k < (A.full_states ? B2S_STATES_REAL_FULL : B2S_STATES_REAL); k++) {
+      B2S_CHECK_PTR(states[k], "state train");
+      A.st[k] = states[k];
+    }
+  }
   if (n == 0) return 0;
   bool sine = flags & B2S_FLAG_SINE_FORM;
   B2S_DISPATCH(launch_real, A, mode, sine, st, s);
@@ -1251,8 +1269,13 @@ int cplx_entry(int64_t n, const double* const ar[4], const double* const ai[4], 
   B2S_CHECK_PTR(smax, "smax"); B2S_CHECK_PTR(smin, "smin"); B2S_CHECK_PTR(shift, "shift");
   A.smax = smax; A.smin = smin; A.shift = shift;
   bool st = flags & B2S_FLAG_STATES;
-  if (st)
-    for (int k = 0; k < B2S_STATES_COMPLEX; k++) { B2S_CHECK_PTR(states[k], "state train"); A.st[k] = states[k]; }
+  if (st) {
+    A.full_states = (flags & B2S_FLAG_STATES_FULL) != 0;
+    for (int k = 0; k < (A.full_states ? B2S_STATES_COMPLEX_FULL : B2S_STATES_COMPLEX); k++) {
+      B2S_CHECK_PTR(states[k], "state train");
+      A.st[k] = states[k];
+    }
+  }
   if (n == 0) return 0;
   bool sine = flags & B2S_FLAG_SINE_FORM;
   B2S_DISPATCH(launch_cplx, A, mode, sine, st, s);

@@ -26,6 +26,9 @@ struct LaneStates {
   double shift, swap_c, swap_r;
   double ph1r, ph1i, ph2r, ph2i, dtr, dti, dhr, dhi;
   double g_tan, g_cos, r11, r12, r22, l_tan, r_tan, smax, smin;
+  // the rest of svd2_lanes' with_states tuple (B2S_FLAG_STATES_FULL)
+  double l_sec2, l_cos, r_sec2, r_cos;
+  double sp[8];                  // ScaleResult.parts, input component order
 };
 
 struct RealOut {
@@ -197,6 +200,7 @@ template <bool Sine, bool States>
 __device__ __forceinline__ void svd2_real_x(const double (&a)[4], RealOut& o, LaneStates* st) {
   double e[4] = {a[0], a[1], a[2], a[3]};            // e11 e21 e12 e22
   double shift = scale_x<4>(e);
+  if (States) for (int t = 0; t < 4; t++) st->sp[t] = e[t];
   // column_norms, svd2.py:167-182
   double m11 = fabs_(e[0]), m21 = fabs_(e[1]), m12 = fabs_(e[2]), m22 = fabs_(e[3]);
   double n1 = hypot_x(m11, m21), n2 = hypot_x(m12, m22);
@@ -231,6 +235,7 @@ __device__ __forceinline__ void svd2_real_x(const double (&a)[4], RealOut& o, La
     st->ph1r = U.ph1; st->ph2r = U.ph2; st->dtr = U.dt; st->dhr = U.dh;
     st->g_tan = neg_(U.mt); st->g_cos = U.cg; st->r11 = r11; st->r12 = r12; st->r22 = r22;
     st->l_tan = T.l_tan; st->r_tan = T.r_tan; st->smax = T.smax; st->smin = T.smin;
+    st->l_sec2 = T.l_sec2; st->l_cos = T.l_cos; st->r_sec2 = T.r_sec2; st->r_cos = T.r_cos;
   }
 }
 
@@ -301,6 +306,7 @@ __device__ __forceinline__ void svd2_complex_x(const double (&ar)[4], const doub
   // component order of svd2_lanes: e11r, e11i, e21r, e21i, e12r, ...
   double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
   double shift = scale_x<8>(p);
+  if (States) for (int t = 0; t < 8; t++) st->sp[t] = p[t];
   double er[4] = {p[0], p[2], p[4], p[6]}, ei[4] = {p[1], p[3], p[5], p[7]};
   // column_norms, svd2.py:176-181
   double m11 = hypot_x(er[0], ei[0]), m21 = hypot_x(er[1], ei[1]);
@@ -346,6 +352,7 @@ __device__ __forceinline__ void svd2_complex_x(const double (&ar)[4], const doub
     st->dtr = U.dtr; st->dti = U.dti; st->dhr = U.dhr; st->dhi = U.dhi;
     st->g_tan = neg_(U.mt); st->g_cos = U.cg; st->r11 = r11; st->r12 = r12; st->r22 = r22;
     st->l_tan = T.l_tan; st->r_tan = T.r_tan; st->smax = T.smax; st->smin = T.smin;
+    st->l_sec2 = T.l_sec2; st->l_cos = T.l_cos; st->r_sec2 = T.r_sec2; st->r_cos = T.r_cos;
   }
 }
 

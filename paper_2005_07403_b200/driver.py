@@ -236,10 +236,10 @@ def run_batch_into(batch, out, cfg, sine_form=False):
 
 def _dump_states(path, batch, sine_form):
     """Raw binary64 state trains, driver.py:193-216 order (outside timing)."""
-    _, states = _svd2.svd2_lanes(batch.parts(), sine_form=sine_form,
-                                 with_states=True)
+    _, scale, urv, tri = _svd2.svd2_lanes(batch.parts(), sine_form=sine_form,
+                                          with_states=True)
     with open(path, "wb") as fh:
-        for train in states.trains():
+        for train in _svd2.dump_trains(scale, urv, tri):
             arr = train.cpu().numpy() if hasattr(train, "cpu") else train
             np.ascontiguousarray(arr, dtype="<f8").tofile(fh)
 

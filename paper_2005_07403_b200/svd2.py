@@ -6,7 +6,8 @@ C-ABI.  Trains may be host NumPy arrays (staged through HBM and returned as
 NumPy) or CUDA tensors (processed in place on their device, results left in
 HBM).  The per-phase helpers of the reference (compute_scale ... assemble_uv)
 have no separate kernels: all phases are fused in registers; their
-intermediate values are exported by ``with_states=True`` instead.
+intermediate values are exported by ``with_states=True`` instead, as the
+reference's (Svd2, ScaleResult, UrvState, TriangleSvd) tuple.
 """
 
 from __future__ import annotations
@@ -18,13 +19,15 @@ import numpy as np
 from . import _lib
 from .layout import is_device_array
 
-__all__ = ["HEADROOM_EXP", "SQRT_DBL_MAX", "Svd2", "LaneStates",
-           "svd2_lanes", "backscale", "launch_device"]
+__all__ = ["HEADROOM_EXP", "SQRT_DBL_MAX", "Svd2", "ScaleResult", "UrvState",
+           "TriangleSvd", "dump_trains", "svd2_lanes", "backscale", "launch_device"]
 
 HEADROOM_EXP = 1021.0                  # svd2.py:52-56
 SQRT_DBL_MAX = 1.34078079299425956e+154  # svd2.py:58-59
 
-# driver.py:193-216 state-train order
+# driver.py:193-216 state-train order (B2S_FLAG_STATES), then the rest of the
+# with_states tuple (B2S_FLAG_STATES_FULL): triangle sec2/cos, scaled parts
+EXTRA_STATE_NAMES = ("left_sec2", "left_cos", "right_sec2", "right_cos")
 STATE_NAMES_REAL = ("shift", "swap_cols", "swap_rows", "row_phase1",
                     "row_phase2", "r12_phase", "r22_phase", "givens_tan",
                     "givens_cos", "r11", "r12", "r22", "left_tan",
@@ -56,12 +59,57 @@ class Svd2:
     shift: object
 
 
-class LaneStates(dict):
-    """Intermediate per-lane quantities of the fused kernel, keyed by the
-    names of driver._dump_states' train order."""
+@dataclass
+class ScaleResult:
+    """svd2.py:61-65: exactly scaled component trains (input order) and the
+    per-lane exponent s."""
+    shift: object
+    parts: tuple
 
-    def trains(self):
-        return list(self.values())
+
+@dataclass
+class UrvState:
+    """svd2.py:68-87: the unitary reduction to a non-negative triangle.
+    Phases are (re, im) pairs (im None for real lanes)."""
+    swap_cols: object
+    swap_rows: object
+    row_phase1: tuple
+    row_phase2: tuple
+    givens_tan: object
+    givens_cos: object
+    r12_phase: tuple
+    r22_phase: tuple
+    r11: object
+    r12: object
+    r22: object
+
+
+@dataclass
+class TriangleSvd:
+    """svd2.py:90-105: closed-form SVD of the triangle."""
+    left_tan: object
+    left_sec2: object
+    left_cos: object
+    right_tan: object
+    right_sec2: object
+    right_cos: object
+    smax_scaled: object
+    smin_scaled: object
+
+
+def dump_trains(scale, urv, tri):
+    """The driver._dump_states train order (driver.py:193-216) of a
+    with_states tuple: shift, swaps as 0.0/1.0, the four phases (re then im
+    for complex lanes), Givens tan/cos, r11, r12, r22, the two tangents and
+    the scaled singular values."""
+    f = lambda m: (m.astype(np.float64) if isinstance(m, np.ndarray) else m.double())
+    trains = [scale.shift, f(urv.swap_cols), f(urv.swap_rows)]
+    for ph in (urv.row_phase1, urv.row_phase2, urv.r12_phase, urv.r22_phase):
+        trains.append(ph[0])
+        if ph[1] is not None:
+            trains.append(ph[1])
+    return trains + [urv.givens_tan, urv.givens_cos, urv.r11, urv.r12, urv.r22,
+                     tri.left_tan, tri.right_tan, tri.smax_scaled, tri.smin_scaled]
 
 
 def _stream_of(t):
@@ -116,8 +164,10 @@ def launch_device(n, in_re, in_im, out, mode, flags=0, states=None,
         groups += [("in_im", in_im), ("u_im", out["u_im"]), ("v_im", out["v_im"])]
     if states is not None:
         groups.append(("states", states))
+    base = len(STATE_NAMES_COMPLEX if cplx else STATE_NAMES_REAL)
+    full = base + len(EXTRA_STATE_NAMES) + (8 if cplx else 4)
     want = {"smax/smin/shift": 3,
-            "states": len(STATE_NAMES_COMPLEX if cplx else STATE_NAMES_REAL)}
+            "states": full if flags & _lib.FLAG_STATES_FULL else base}
     for what, trains in groups:
         if len(trains) != want.get(what, 4):
             raise ValueError("%s: expected %d trains, got %d"
@@ -162,8 +212,9 @@ def svd2_lanes(parts, sine_form=False, with_states=False, device=None):
     """Full pipeline on component trains (svd2.py:521-570).
 
     parts: 4 trains (e11, e21, e12, e22) for real lanes or 8 with re/im
-    interleaved per entry.  Returns ``Svd2`` (and ``LaneStates`` when
-    ``with_states``); host inputs give host results."""
+    interleaved per entry.  Returns ``Svd2``, or with ``with_states`` the
+    reference's ``(Svd2, ScaleResult, UrvState, TriangleSvd)``; host inputs
+    give host (NumPy) results, device inputs device tensors."""
     import torch
     if len(parts) not in (4, 8):
         raise ValueError("expected 4 or 8 component trains, got %d"
@@ -187,10 +238,12 @@ def svd2_lanes(parts, sine_form=False, with_states=False, device=None):
            "u_im": [E() for _ in range(4)] if cplx else None,
            "v_im": [E() for _ in range(4)] if cplx else None,
            "smax": E(), "smin": E(), "shift": E()}
-    names = STATE_NAMES_COMPLEX if cplx else STATE_NAMES_REAL
-    states = [E() for _ in names] if with_states else None
-    launch_device(n, in_re, in_im, out, 0,
-                  _lib.FLAG_SINE_FORM if sine_form else 0, states)
+    names = (STATE_NAMES_COMPLEX if cplx else STATE_NAMES_REAL) + EXTRA_STATE_NAMES
+    states = [E() for _ in range(len(names) + len(parts))] if with_states else None
+    flags = _lib.FLAG_SINE_FORM if sine_form else 0
+    if with_states:
+        flags |= _lib.FLAG_STATES_FULL
+    launch_device(n, in_re, in_im, out, 0, flags, states)
     fin = (lambda t: t.cpu().numpy()) if host else (lambda t: t)
     pair = lambda k: (fin(out["u_re"][k]), fin(out["u_im"][k]) if cplx else None)
     vpair = lambda k: (fin(out["v_re"][k]), fin(out["v_im"][k]) if cplx else None)
@@ -198,9 +251,23 @@ def svd2_lanes(parts, sine_form=False, with_states=False, device=None):
                v11=vpair(0), v21=vpair(1), v12=vpair(2), v22=vpair(3),
                smax_scaled=fin(out["smax"]), smin_scaled=fin(out["smin"]),
                shift=fin(out["shift"]))
-    if with_states:
-        return svd, LaneStates(zip(names, [fin(s) for s in states]))
-    return svd
+    if not with_states:
+        return svd
+    st = dict(zip(names, [fin(x) for x in states[:len(names)]]))
+    scaled = tuple(fin(x) for x in states[len(names):])
+    ph = lambda k: (st[k + "_re"], st[k + "_im"]) if cplx else (st[k], None)
+    mask = lambda x: (x != 0.0)
+    scale = ScaleResult(shift=st["shift"], parts=scaled)
+    urv = UrvState(swap_cols=mask(st["swap_cols"]), swap_rows=mask(st["swap_rows"]),
+                   row_phase1=ph("row_phase1"), row_phase2=ph("row_phase2"),
+                   givens_tan=st["givens_tan"], givens_cos=st["givens_cos"],
+                   r12_phase=ph("r12_phase"), r22_phase=ph("r22_phase"),
+                   r11=st["r11"], r12=st["r12"], r22=st["r22"])
+    tri = TriangleSvd(left_tan=st["left_tan"], left_sec2=st["left_sec2"],
+                      left_cos=st["left_cos"], right_tan=st["right_tan"],
+                      right_sec2=st["right_sec2"], right_cos=st["right_cos"],
+                      smax_scaled=st["smax_scaled"], smin_scaled=st["smin_scaled"])
+    return svd, scale, urv, tri
 
 
 def backscale(smax_scaled, smin_scaled, shift, mode="safe"):

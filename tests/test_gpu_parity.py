@@ -22,6 +22,7 @@ import oracle  # noqa: E402
 import paper_2005_07403_b200 as b2s  # noqa: E402
 from paper_2005_07403_b200 import _lib, synth  # noqa: E402
 from paper_2005_07403_b200.layout import Batch2x2, from_trains  # noqa: E402
+from paper_2005_07403_b200.svd2 import dump_trains  # noqa: E402
 
 DEV = torch.device("cuda", 0)
 RECORD_MODES = {"patterned_real_safe": ("safe", False),
@@ -78,9 +79,34 @@ def test_state_dump_matches_reference(lanes):
         parts = [rec["in_re"][t] for t in range(4)]
         if "in_im" in rec:
             parts = [x for t in range(4) for x in (rec["in_re"][t], rec["in_im"][t])]
-        _, states = b2s.svd2_lanes(tuple(parts), with_states=True)
-        got = np.stack(states.trains())
+        _, scale, urv, tri = b2s.svd2_lanes(tuple(parts), with_states=True)
+        got = np.stack(dump_trains(scale, urv, tri))
         assert_bits_equal(got, rec["states"], name + "/states")
+
+
+def test_with_states_tuple_matches_reference(lanes):
+    """svd2_lanes(with_states=True) returns the reference's
+    (Svd2, ScaleResult, UrvState, TriangleSvd) (svd2.py:568-569): every
+    field bit-identical to lanesvd's own on the golden lane sets -- the
+    dump trains (lanes.npz) and the scaled parts and triangle sec2 / cos
+    (states_full.npz, make_states_full.py)."""
+    full = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                "states_full.npz"))
+    for name, rec in lanes.items():
+        if "states" not in rec:
+            continue
+        parts = [rec["in_re"][t] for t in range(4)]
+        if "in_im" in rec:
+            parts = [x for t in range(4) for x in (rec["in_re"][t], rec["in_im"][t])]
+        svd, scale, urv, tri = b2s.svd2_lanes(tuple(parts), with_states=True)
+        assert isinstance(scale, b2s.ScaleResult) and isinstance(urv, b2s.UrvState)
+        assert isinstance(tri, b2s.TriangleSvd)
+        assert urv.swap_cols.dtype == np.bool_ and len(scale.parts) == len(parts)
+        assert (urv.row_phase1[1] is None) == ("in_im" not in rec)
+        assert_bits_equal(np.stack(scale.parts), full[name + "/scaled_parts"], name + "/parts")
+        assert_bits_equal(np.stack([tri.left_sec2, tri.left_cos, tri.right_sec2, tri.right_cos]),
+                          full[name + "/tri"], name + "/tri")
+        assert_bits_equal(tri.smax_scaled, svd.smax_scaled, name + "/smax")
 
 
 @pytest.mark.parametrize("config", [0, 1, 2])
@@ -456,7 +482,7 @@ def test_theorem1_invariants_full_range_fuzz(field):
     rng = np.random.default_rng(2026 if field == "real" else 2027)
     ntr = 4 if field == "real" else 8
     parts = tuple(torch.from_numpy(_random_finite(rng, n)).to(DEV) for _ in range(ntr))
-    svd, st = b2s.svd2_lanes(parts, with_states=True)
+    svd, _scale, urv, tri = b2s.svd2_lanes(parts, with_states=True)
     re = torch.stack(parts[0::2] if ntr == 8 else parts)
     im = torch.stack(parts[1::2]) if ntr == 8 else None
     fast, _ = b2s.run_batch(b2s.Batch2x2(n=n, re=re, im=im), b2s.RunConfig(field=field))
@@ -465,12 +491,12 @@ def test_theorem1_invariants_full_range_fuzz(field):
     assert_bits_equal(smin, svd.smin_scaled.cpu().numpy(), "smin fast vs state-dump kernel")
     assert np.isfinite(smax).all() and np.isfinite(smin).all()
     assert (smax >= smin).all() and (smin >= 0.0).all()
-    lt = st["left_tan"].cpu().numpy()
-    rt = st["right_tan"].cpu().numpy()
+    lt = tri.left_tan.cpu().numpy()
+    rt = tri.right_tan.cpu().numpy()
     assert (np.abs(rt) <= np.sqrt(2.0) * (1 + 2 * eps)).all()
     assert (np.abs(rt) >= np.abs(lt)).all()
     # cos psi is V's (1,1) entry before the column swap (svd2.py:350-369)
-    swap_c = st["swap_cols"].cpu().numpy() != 0
+    swap_c = urv.swap_cols.cpu().numpy()
     v11, v21 = np.abs(svd.v11[0].cpu().numpy()), np.abs(svd.v21[0].cpu().numpy())
     rc = np.where(swap_c, v21, v11)
     assert (rc >= (1 / np.sqrt(3.0)) * (1 - 2 * eps)).all()

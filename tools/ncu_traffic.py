@@ -25,6 +25,9 @@ def kernels(path):
             return float(d[k].replace(",", "")) * scale.get(u[k], 1)
         out.append({"kernel": d["Kernel Name"], "read": val("dram__bytes_read.sum"),
                     "write": val("dram__bytes_write.sum"),
+                    "inst": val("smsp__inst_executed.sum"),
+                    "fp64_pipe_pct": val("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                    "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                     "time_ms": float(d["gpu__time_duration.sum"].replace(",", "")) *
                     {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(u["gpu__time_duration.sum"], 1)})
     return out
@@ -38,11 +41,15 @@ def main():
         config, lanes, path = a[k], int(a[k + 1]), a[k + 2]
         ks = kernels(path)
         tot = sum(x["read"] + x["write"] for x in ks)
+        main_k = [x for x in ks if "k_svd2" in x["kernel"]][0]
         res[config] = {"bytes_per_lane": tot / lanes, "lanes_profiled": lanes, "report": os.path.basename(path),
+                       "fp64_pipe_pct": main_k["fp64_pipe_pct"],
+                       "issue_active_pct": main_k["issue_active_pct"],
+                       "instr_per_lane": round(main_k["inst"] * 32 / lanes, 1),
                        "kernels": ks}
     with open(OUT, "w") as fh:
         json.dump(res, fh, indent=1)
-    print(json.dumps({k: v["bytes_per_lane"] for k, v in res.items()}))
+    print(json.dumps({k: v["bytes_per_lane"] for k, v in res.items() if isinstance(v, dict)}))
 
 
 if __name__ == "__main__":

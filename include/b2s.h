@@ -148,6 +148,17 @@ int b2s_synth(int config, uint64_t seed, int64_t lane0, int64_t n,
               double *const re[4], double *const im[4], void *stream);
 
 /*
+ * lanesvd.verify.oracle_svd2 (verify.py:259-352) on the device: the
+ * closed-form double-double reference SVD of n matrices given as trains
+ * (a_im NULL for real input), bit-identical to the reference's.  out[36]:
+ * smax hi/lo, smin hi/lo, then u11 u21 u12 u22 v11 v21 v12 v22 as
+ * re.hi re.lo im.hi im.lo (n doubles each).
+ */
+int b2s_oracle_svd2(int64_t n, const double *const a_re[4],
+                    const double *const a_im[4], double *const out[36],
+                    void *stream);
+
+/*
  * Batch quality metrics in double-double (lanesvd.verify.metrics,
  * verify.py:355-477), bit-identical per lane to the reference: relative
  * residual rho, unitarity defects delta (U) and eta (V), condition number

@@ -16,7 +16,7 @@ from .driver import RunConfig, run_batch, run_batch_into, shards, svd2_chunk, sv
 from .layout import (LANE_WIDTH, Batch2x2, MatrixSvd, SvdBatchOut, aligned_zeros,
                      from_trains, pack, padded_len, unpack, unpack_inputs)
 from .svd2 import ScaleResult, Svd2, TriangleSvd, UrvState, backscale, svd2_lanes
-from .verify import Metrics, metrics
+from .verify import Metrics, metrics, oracle_svd2
 
 # lanesvd's package namespace (lanesvd/__init__.py) plus this engine's extras
 __all__ = sorted([
@@ -24,7 +24,7 @@ __all__ = sorted([
     "RunConfig", "run_batch", "svd2_chunk", "svd2_single", "Metrics", "metrics",
     "aligned_zeros", "pack", "unpack", "unpack_inputs", "from_trains",
     "run_batch_into", "shards", "Svd2", "svd2_lanes", "backscale",
-    "ScaleResult", "UrvState", "TriangleSvd",
+    "ScaleResult", "UrvState", "TriangleSvd", "oracle_svd2",
     "assert_device_fp_env", "LIB_PATH",
 ])
 

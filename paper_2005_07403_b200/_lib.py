@@ -35,6 +35,7 @@ SYMBOLS = (
     "b2s_synth", "b2s_check_fp_env", "b2s_math_probe",
     "b2s_reserve_workspace", "b2s_hard_lane_count",
     "b2s_svd2_real_records", "b2s_svd2_complex_records", "b2s_metrics",
+    "b2s_oracle_svd2",
 )
 
 _P = ctypes.c_void_p
@@ -74,6 +75,7 @@ def _load():
     L.b2s_svd2_complex_records.argtypes = [_i64, _P, _PA, _PA, _PA, _PA, _P,
                                            _P, _P, _int, _int, _P]
     L.b2s_hard_lane_count.argtypes = [_int]
+    L.b2s_oracle_svd2.argtypes = [_i64, _PA, _PA, _PA, _P]
     for name in SYMBOLS:
         if name not in ("b2s_version", "b2s_last_error"):
             getattr(L, name).restype = _int

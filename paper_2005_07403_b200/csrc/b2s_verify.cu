@@ -311,9 +311,124 @@ __global__ void __launch_bounds__(kMBlock) k_metrics(const MetricArgs M) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// lanesvd.verify.oracle_svd2 (verify.py:259-352): the closed-form reference
+// SVD in double-double, independent of the pipeline phases -- per lane an
+// exact power-of-two prescale by the largest component's exponent, the Gram
+// matrix's eigensystem with the cancellation-free discriminant, smin from
+// |det| / smax, the right vectors from the better-conditioned Gram row, the
+// left vectors as their images (the unitary completion when smin / smax <
+// 1e-25).  The same double-double operation sequence as the reference, so
+// every output word is bit-identical.  Output trains (36): smax hi/lo, smin
+// hi/lo, then u11 u21 u12 u22 v11 v21 v12 v22 as re.hi re.lo im.hi im.lo.
+// ---------------------------------------------------------------------------
+struct OracleArgs {
+  int64_t n;
+  int cplx;
+  const double* ar[4];
+  const double* ai[4];
+  double* out[36];
+};
+
+namespace dd {
+__device__ __forceinline__ DD sel(bool m, DD a, DD b) { return m ? a : b; }
+__device__ __forceinline__ CD csel(bool m, CD a, CD b) { return m ? a : b; }
+__device__ __forceinline__ CD cdiv_dd(CD a, DD s) { return {div(a.re, s), div(a.im, s)}; }
+}  // namespace dd
+
+__global__ void __launch_bounds__(128) k_oracle_svd2(const OracleArgs O) {
+  using namespace dd;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < O.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double re[4], im[4];
+    double mags = 0.0, mi = 0.0;
+    for (int t = 0; t < 4; t++) {
+      re[t] = O.ar[t][i];
+      im[t] = O.cplx ? O.ai[t][i] : 0.0;
+      mags = fmax(mags, fabs(re[t]));
+      mi = fmax(mi, fabs(im[t]));
+    }
+    mags = fmax(mags, mi);
+    const double g = mags > 0.0 ? getexp_dev(mags) : 0.0;
+    CD e[4];                                        // e11, e21, e12, e22
+    for (int t = 0; t < 4; t++) e[t] = cfrom(scalef_dev(re[t], -g), scalef_dev(im[t], -g));
+    const DD m11 = add(abs2(e[0]), abs2(e[1]));
+    const DD m22 = add(abs2(e[2]), abs2(e[3]));
+    const CD m12 = cadd(cmul(conj(e[0]), e[2]), cmul(conj(e[1]), e[3]));
+    const DD trace = add(m11, m22);
+    const DD diff = sub(m11, m22);
+    const DD disc = sqrt(add(mul(diff, diff), scalb(abs2(m12), 2.0)));
+    const DD lam_max = scalb(add(trace, disc), -1.0);
+    DD smax = sqrt(lam_max);
+    const CD det = csub(cmul(e[0], e[3]), cmul(e[2], e[1]));
+    const DD absdet = sqrt(abs2(det));
+    const bool zero_s = smax.hi == 0.0;
+    const DD z = from(0.0), one = from(1.0);
+    DD smin = sel(zero_s, z, div(absdet, smax));
+    const bool big1 = m11.hi >= m22.hi;
+    CD v11 = csel(big1, CD{sub(lam_max, m22), z}, m12);
+    CD v21 = csel(big1, conj(m12), CD{sub(lam_max, m11), z});
+    const DD nrm2 = add(abs2(v11), abs2(v21));
+    const bool degen = nrm2.hi == 0.0;
+    v11 = csel(degen, CD{one, z}, v11);
+    v21 = csel(degen, CD{z, z}, v21);
+    const DD nrm = sqrt(sel(degen, one, nrm2));
+    v11 = cdiv_dd(v11, nrm);
+    v21 = cdiv_dd(v21, nrm);
+    const CD v12 = {neg(v21.re), v21.im};
+    const CD v22 = conj(v11);
+    const CD av1 = cadd(cmul(e[0], v11), cmul(e[2], v21));
+    const CD av2 = cadd(cmul(e[1], v11), cmul(e[3], v21));
+    const DD safe_smax = sel(zero_s, one, smax);
+    const CD u11 = csel(zero_s, CD{one, z}, cdiv_dd(av1, safe_smax));
+    const CD u21 = csel(zero_s, CD{z, z}, cdiv_dd(av2, safe_smax));
+    const CD bv1 = cadd(cmul(e[0], v12), cmul(e[2], v22));
+    const CD bv2 = cadd(cmul(e[1], v12), cmul(e[3], v22));
+    const bool reliable = smin.hi > __dmul_rn(smax.hi, 1e-25);
+    const DD safe_smin = sel(reliable, smin, one);
+    const CD u12 = csel(reliable, cdiv_dd(bv1, safe_smin), CD{neg(u21.re), u21.im});
+    const CD u22 = csel(reliable, cdiv_dd(bv2, safe_smin), conj(u11));
+    smax = scalb(smax, g);
+    smin = scalb(smin, g);
+    double* const* o = O.out;
+    o[0][i] = smax.hi; o[1][i] = smax.lo; o[2][i] = smin.hi; o[3][i] = smin.lo;
+    const CD f[8] = {u11, u21, u12, u22, v11, v21, v12, v22};
+    for (int k = 0; k < 8; k++) {
+      o[4 + 4 * k][i] = f[k].re.hi;
+      o[5 + 4 * k][i] = f[k].re.lo;
+      o[6 + 4 * k][i] = f[k].im.hi;
+      o[7 + 4 * k][i] = f[k].im.lo;
+    }
+  }
+}
+
 }  // namespace b2s
 
 using namespace b2s;
+
+extern "C" int b2s_oracle_svd2(int64_t n, const double* const a_re[4], const double* const a_im[4],
+                               double* const out[36], void* stream) {
+  if (n < 0) return fail(1, "negative batch size");
+  if (!a_re || !out) return fail(5, "NULL argument");
+  OracleArgs O{};
+  O.n = n;
+  O.cplx = a_im != nullptr;
+  for (int t = 0; t < 4; t++) {
+    if (!a_re[t] || (O.cplx && !a_im[t])) return fail(5, "NULL input train");
+    O.ar[t] = a_re[t];
+    if (O.cplx) O.ai[t] = a_im[t];
+  }
+  for (int k = 0; k < 36; k++) {
+    if (!out[k]) return fail(5, "NULL output train");
+    O.out[k] = out[k];
+  }
+  if (n == 0) return 0;
+  int blocks = (int)((n + 127) / 128);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_oracle_svd2<<<blocks, 128, 0, (cudaStream_t)stream>>>(O);
+  B2S_CUDA(cudaGetLastError());
+  return 0;
+}
 
 extern "C" int b2s_metrics(int64_t n, const double* const a_re[4], const double* const a_im[4],
                            const double* const u_re[4], const double* const u_im[4],

@@ -13,13 +13,15 @@ lanes/s/core) it covers a 2^30-lane batch in one pass.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 
 from . import _lib
 from .layout import is_device_array
 
-__all__ = ["Metrics", "metrics", "lane_metrics", "fold_partials"]
+__all__ = ["Metrics", "metrics", "lane_metrics", "fold_partials", "DD", "OracleSvd",
+           "oracle_svd2"]
 
 _NPART = 17
 
@@ -125,3 +127,85 @@ def lane_metrics(batch, out):
     folded batch record."""
     p, lanes = _run(batch, out, True)
     return lanes, fold_partials(p)
+
+
+# ---------------------------------------------------------------------------
+# independent reference SVD (verify.py:222-352)
+# ---------------------------------------------------------------------------
+
+class DD(NamedTuple):
+    """Double-double values (verify.py:42-45): hi + lo, |lo| <= ulp(hi)/2."""
+    hi: np.ndarray
+    lo: np.ndarray
+
+
+@dataclass
+class OracleSvd:
+    """Reference factors in double-double, one lane per array slot
+    (verify.py:222-252): ``smax``/``smin`` DD arrays; factor entries complex
+    double-double pairs (DD re, DD im), imaginary parts exactly zero for real
+    input."""
+    smax: DD
+    smin: DD
+    u11: tuple
+    u21: tuple
+    u12: tuple
+    u22: tuple
+    v11: tuple
+    v21: tuple
+    v12: tuple
+    v22: tuple
+
+    def u_array(self, k):
+        return _factor_array((self.u11, self.u12, self.u21, self.u22), k)
+
+    def v_array(self, k):
+        return _factor_array((self.v11, self.v12, self.v21, self.v22), k)
+
+
+def _factor_array(entries, k):
+    vals = [complex(float(e[0].hi[k]) + float(e[0].lo[k]),
+                    float(e[1].hi[k]) + float(e[1].lo[k])) for e in entries]
+    return np.array([[vals[0], vals[1]], [vals[2], vals[3]]])
+
+
+def oracle_svd2(matrices, device=None):
+    """Closed-form reference SVD of 2x2 lanes in double-double
+    (lanesvd.verify.oracle_svd2, verify.py:259-352), computed on the GPU by
+    ``b2s_oracle_svd2`` with the reference's own double-double operation
+    sequence -- every output word bit-identical.  Accepts one (2, 2) matrix
+    or an (n, 2, 2) stack, real or complex; returns host arrays."""
+    import torch
+    a = np.asarray(matrices)
+    if a.shape == (2, 2):
+        a = a.reshape(1, 2, 2)
+    if a.ndim != 3 or a.shape[1:] != (2, 2):
+        raise ValueError("expected (n, 2, 2) matrices, got %r" % (a.shape,))
+    cplx = bool(np.iscomplexobj(a))
+    if cplx:
+        a = a.astype(np.complex128, copy=False)
+        parts_re, parts_im = a.real, a.imag
+    else:
+        parts_re, parts_im = a.astype(np.float64, copy=False), None
+    n = a.shape[0]
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    # trains in column-major entry order: e11, e21, e12, e22 (layout.py:3-10)
+    order = ((0, 0), (1, 0), (0, 1), (1, 1))
+    up = lambda p: torch.from_numpy(np.ascontiguousarray(
+        np.stack([p[:, i, j] for i, j in order]), dtype=np.float64)).to(device)
+    tre = up(parts_re)
+    tim = up(parts_im) if cplx else None
+    out = torch.empty((36, max(n, 1)), dtype=torch.float64, device=device)
+    ar, k1 = _lib.ptr_array([tre[t].data_ptr() for t in range(4)])
+    ai, k2 = (None, None) if tim is None else _lib.ptr_array([tim[t].data_ptr() for t in range(4)])
+    op, k3 = _lib.ptr_array([out[k].data_ptr() for k in range(36)])
+    with torch.cuda.device(device):
+        rc = _lib.lib.b2s_oracle_svd2(n, ar, ai, op, torch.cuda.current_stream(device).cuda_stream)
+    _lib.check(rc, "b2s_oracle_svd2")
+    h = out[:, :n].cpu().numpy()
+    dd = lambda k: DD(h[k].copy(), h[k + 1].copy())
+    cd = lambda k: (dd(4 + 4 * k), dd(6 + 4 * k))
+    return OracleSvd(smax=dd(0), smin=dd(2), u11=cd(0), u21=cd(1), u12=cd(2), u22=cd(3),
+                     v11=cd(4), v21=cd(5), v12=cd(6), v22=cd(7))

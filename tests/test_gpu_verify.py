@@ -90,3 +90,22 @@ def test_8eps_gate_counts_equal_the_reference():
             out, _ = b2s.run_batch(b, b2s.RunConfig(field=b.field))
             total += fold_partials(_run(b, out, False)[0])["over_8eps_frobenius"]
         assert total == rec["over_8eps_frobenius"], (name, total, rec["over_8eps_frobenius"])
+
+
+def test_oracle_svd2_bit_identical_to_reference():
+    """b2s.oracle_svd2 (the reference's independent double-double SVD,
+    verify.py:259-352, on the GPU): every output word equals lanesvd's own
+    on its test matrices and 2x4096 wide-range real / complex ones
+    (tests/golden/oracle_svd2.npz, make_oracle_svd2.py)."""
+    from helpers import assert_bits_equal
+    g = np.load(os.path.join(GOLDEN, "oracle_svd2.npz"))
+    names = sorted({k.split("/")[0] for k in g.files})
+    for name in names:
+        res = b2s.oracle_svd2(g[name + "/in"])
+        got = [res.smax.hi, res.smax.lo, res.smin.hi, res.smin.lo]
+        for e in (res.u11, res.u21, res.u12, res.u22, res.v11, res.v21, res.v12, res.v22):
+            got += [e[0].hi, e[0].lo, e[1].hi, e[1].lo]
+        assert_bits_equal(np.stack(got), g[name + "/out"], name)
+    one = b2s.oracle_svd2(np.array([[3.0, 0.0], [0.0, -2.0]]))       # single (2, 2) matrix
+    assert one.smax.hi[0] == 3.0 and one.smin.hi[0] == 2.0
+    assert one.u_array(0).shape == (2, 2)

@@ -148,6 +148,40 @@ int b2s_synth(int config, uint64_t seed, int64_t lane0, int64_t n,
               double *const re[4], double *const im[4], void *stream);
 
 /*
+ * One pipeline phase of svd2_lanes on its own (svd2.py:134-474), exact
+ * arithmetic, bit-identical to the reference's phase function for every
+ * finite input: the svd2 module API (compute_scale ... assemble_uv) on the
+ * device.  K = 1 train per value for real lanes, 2 (re, im) for complex;
+ * entries are e11, e21, e12, e22; masks are 0.0 / 1.0.
+ *   phase                      inputs                      outputs
+ *   COMPUTE_SCALE      parts (4K)                  shift, scaled parts (4K)
+ *   COLUMN_NORMS       entries (4K)                m11 m21 m12 m22 n1 n2
+ *   COLUMN_PIVOT       entries, mags (4), n1, n2   entries, mags, n1, n2, swap
+ *   ROW_SORT           entries, mags (4)           entries, mags, swap
+ *   LEFT_PHASE_REDUCE  entries, m11, m21           b11 b21 f12 (K) f22 (K) ph1 (K) ph2 (K)
+ *   GIVENS_QR          b11 b21 f12 (K) f22 (K) n1  tan cos r11 g12 (K) g22 (K)
+ *   PHASE_FIX_R        g12 (K) g22 (K)             r12 r22 r12_phase (K) r22_phase (K)
+ *   TRIANGULAR_SVD     r11 r12 r22                 ltan lsec2 lcos rtan rsec2 rcos smax smin
+ *   ASSEMBLE_UV        swap_cols swap_rows ph1 (K) ph2 (K) givens_tan givens_cos
+ *                      r12_phase (K) r22_phase (K) r11 r12 r22, the 8 triangle
+ *                      trains, shift               u (4K) v (4K) smax smin shift
+ * sine_form selects assemble_uv_sine (svd2.py:427-474).  Device pointers.
+ */
+#define B2S_PHASE_COMPUTE_SCALE 0
+#define B2S_PHASE_COLUMN_NORMS 1
+#define B2S_PHASE_COLUMN_PIVOT 2
+#define B2S_PHASE_ROW_SORT 3
+#define B2S_PHASE_LEFT_PHASE_REDUCE 4
+#define B2S_PHASE_GIVENS_QR 5
+#define B2S_PHASE_PHASE_FIX_R 6
+#define B2S_PHASE_TRIANGULAR_SVD 7
+#define B2S_PHASE_ASSEMBLE_UV 8
+#define B2S_PHASE_MAX_TRAINS 32
+int b2s_svd2_phase(int phase, int complex_field, int sine_form, int64_t n,
+                   int n_in, const double *const *in, int n_out,
+                   double *const *out, void *stream);
+
+/*
  * lanesvd.verify.oracle_svd2 (verify.py:259-352) on the device: the
  * closed-form double-double reference SVD of n matrices given as trains
  * (a_im NULL for real input), bit-identical to the reference's.  out[36]:

@@ -4,10 +4,11 @@
 (svd2.py:521-570, 481-514) but run the fused sm_100a kernels through the
 C-ABI.  Trains may be host NumPy arrays (staged through HBM and returned as
 NumPy) or CUDA tensors (processed in place on their device, results left in
-HBM).  The per-phase helpers of the reference (compute_scale ... assemble_uv)
-have no separate kernels: all phases are fused in registers; their
-intermediate values are exported by ``with_states=True`` instead, as the
-reference's (Svd2, ScaleResult, UrvState, TriangleSvd) tuple.
+HBM).  The batch path fuses every phase in registers; its intermediate values are
+exported by ``with_states=True`` as the reference's (Svd2, ScaleResult,
+UrvState, TriangleSvd) tuple.  The phases also exist one at a time, with the
+reference's signatures (compute_scale ... assemble_uv_sine), each one device
+kernel over the same exact lane arithmetic (``b2s_svd2_phase``).
 """
 
 from __future__ import annotations
@@ -20,7 +21,10 @@ from . import _lib
 from .layout import is_device_array
 
 __all__ = ["HEADROOM_EXP", "SQRT_DBL_MAX", "Svd2", "ScaleResult", "UrvState",
-           "TriangleSvd", "dump_trains", "svd2_lanes", "backscale", "launch_device"]
+           "TriangleSvd", "dump_trains", "svd2_lanes", "backscale", "launch_device",
+           "compute_scale", "column_norms", "column_pivot", "row_sort",
+           "left_phase_reduce", "givens_qr", "phase_fix_r", "triangular_svd",
+           "assemble_uv", "assemble_uv_sine"]
 
 HEADROOM_EXP = 1021.0                  # svd2.py:52-56
 SQRT_DBL_MAX = 1.34078079299425956e+154  # svd2.py:58-59
@@ -295,3 +299,162 @@ def backscale(smax_scaled, smin_scaled, shift, mode="safe"):
     if host:
         return tuple(o.cpu().numpy() for o in outs)
     return tuple(outs)
+
+
+# ---------------------------------------------------------------------------
+# The pipeline's phases one at a time (svd2.py:134-474): the reference's
+# svd2 module API over b2s_svd2_phase.  Values are host NumPy arrays or
+# device tensors (results come back where the inputs live); complex values
+# are (re, im) pairs, real ones (x, None) as in the reference.
+# ---------------------------------------------------------------------------
+
+_PHASE = {"compute_scale": 0, "column_norms": 1, "column_pivot": 2, "row_sort": 3,
+          "left_phase_reduce": 4, "givens_qr": 5, "phase_fix_r": 6,
+          "triangular_svd": 7, "assemble_uv": 8}
+
+
+def _phase(name, cplx, ins, n_out, sine=False, finite=False):
+    """Run one phase kernel on the trains `ins`; returns `n_out` trains."""
+    import torch
+    host = not any(is_device_array(x) for x in ins)
+    dev = next((x.device for x in ins if is_device_array(x)), None)
+    if dev is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+    def up(x):
+        if is_device_array(x):
+            return x.to(device=dev, dtype=torch.float64).reshape(-1).contiguous()
+        a = np.asarray(x)
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).reshape(-1)).to(dev)
+    t = [up(x) for x in ins]
+    n = int(t[0].numel())
+    if any(int(x.numel()) != n for x in t):
+        raise ValueError("%s: trains must be equal-length vectors" % name)
+    if finite and not all(bool(torch.isfinite(x).all()) for x in t):
+        raise ValueError("%s: non-finite component" % name)
+    _lib.assert_device_fp_env(dev.index or 0)
+    outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(n_out)]
+    pi, _k1 = _lib.ptr_array([x.data_ptr() for x in t])
+    po, _k2 = _lib.ptr_array([x.data_ptr() for x in outs])
+    with torch.cuda.device(dev):
+        rc = _lib.lib.b2s_svd2_phase(_PHASE[name], int(cplx), int(sine), n, len(t), pi,
+                                     len(outs), po, torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(rc, "b2s_svd2_phase(%s)" % name)
+    if host:
+        return [x.cpu().numpy() for x in outs]
+    return outs
+
+
+def _flat(pairs):
+    """(re, im|None) pairs -> trains, and whether they are complex."""
+    cplx = pairs[0][1] is not None
+    if any((p[1] is not None) != cplx for p in pairs):
+        raise ValueError("mixed real and complex values")
+    return [x for p in pairs for x in ((p[0], p[1]) if cplx else (p[0],))], cplx
+
+
+def _pairs(trains, cplx, count):
+    k = 2 if cplx else 1
+    return tuple((trains[k * j], trains[k * j + 1] if cplx else None) for j in range(count))
+
+
+def _mask(x):
+    return x != 0.0
+
+
+def compute_scale(parts):
+    """Joint exact power-of-two scaling (svd2.py:134-160) of 4 real or 8
+    complex component trains; finite components (as the batch path
+    requires).  Returns ``ScaleResult``."""
+    if len(parts) not in (4, 8):
+        raise ValueError("expected 4 or 8 component trains, got %d" % len(parts))
+    out = _phase("compute_scale", len(parts) == 8, list(parts), 1 + len(parts), finite=True)
+    return ScaleResult(shift=out[0], parts=tuple(out[1:]))
+
+
+def column_norms(e11, e21, e12, e22):
+    """Entry magnitudes and column norms (svd2.py:167-182):
+    ``(m11, m21, m12, m22, norm1, norm2)``."""
+    tr, cplx = _flat((e11, e21, e12, e22))
+    return tuple(_phase("column_norms", cplx, tr, 6))
+
+
+def column_pivot(entries, mags, norm1, norm2):
+    """Exchange columns where norm1 < norm2 (svd2.py:193-208): returns
+    ``(entries, mags, n1, n2, swap)``."""
+    tr, cplx = _flat(entries)
+    k = len(tr)
+    out = _phase("column_pivot", cplx, tr + list(mags) + [norm1, norm2], k + 7)
+    return (_pairs(out, cplx, 4), tuple(out[k:k + 4]), out[k + 4], out[k + 5],
+            _mask(out[k + 6]))
+
+
+def row_sort(entries, mags):
+    """Exchange rows where m11 < m21 (svd2.py:211-224): returns
+    ``(entries, mags, swap)``."""
+    tr, cplx = _flat(entries)
+    k = len(tr)
+    out = _phase("row_sort", cplx, tr + list(mags), k + 5)
+    return _pairs(out, cplx, 4), tuple(out[k:k + 4]), _mask(out[k + 4])
+
+
+def left_phase_reduce(e11, e21, e12, e22, m11, m21):
+    """Row phases of the pivot column (svd2.py:227-250): returns
+    ``(b11, b21, f12, f22, phase1, phase2)``."""
+    tr, cplx = _flat((e11, e21, e12, e22))
+    out = _phase("left_phase_reduce", cplx, tr + [m11, m21], 2 + len(tr))
+    f12, f22, ph1, ph2 = _pairs(out[2:], cplx, 4)
+    return out[0], out[1], f12, f22, ph1, ph2
+
+
+def givens_qr(b11, b21, f12, f22, norm1):
+    """One rotation annihilating the subdiagonal (svd2.py:253-276):
+    returns ``(tan, cos, r11, g12, g22)``."""
+    tr, cplx = _flat((f12, f22))
+    out = _phase("givens_qr", cplx, [b11, b21] + tr + [norm1], 3 + len(tr))
+    g12, g22 = _pairs(out[3:], cplx, 2)
+    return out[0], out[1], out[2], g12, g22
+
+
+def phase_fix_r(g12, g22):
+    """Strip the phases of the rotated column 2 (svd2.py:279-299): returns
+    ``(r12, r22, r12_phase, r22_phase)``."""
+    tr, cplx = _flat((g12, g22))
+    out = _phase("phase_fix_r", cplx, tr, 2 + len(tr))
+    dt, dh = _pairs(out[2:], cplx, 2)
+    return out[0], out[1], dt, dh
+
+
+def triangular_svd(r11, r12, r22):
+    """Closed-form SVD of the non-negative triangle (svd2.py:306-343)."""
+    out = _phase("triangular_svd", False, [r11, r12, r22], 8)
+    return TriangleSvd(*out)
+
+
+def _assemble(urv, tri, shift, sine):
+    tr, cplx = _flat((urv.row_phase1, urv.row_phase2))
+    ph = tr
+    dtr, _ = _flat((urv.r12_phase, urv.r22_phase))
+    f = lambda m: (m.astype(np.float64) if isinstance(m, np.ndarray) else
+                   m.double() if hasattr(m, "double") else np.asarray(m, dtype=np.float64))
+    ins = ([f(urv.swap_cols), f(urv.swap_rows)] + ph + [urv.givens_tan, urv.givens_cos] + dtr +
+           [urv.r11, urv.r12, urv.r22, tri.left_tan, tri.left_sec2, tri.left_cos, tri.right_tan,
+            tri.right_sec2, tri.right_cos, tri.smax_scaled, tri.smin_scaled, shift])
+    k = 2 if cplx else 1
+    out = _phase("assemble_uv", cplx, ins, 8 * k + 3, sine=sine)
+    u = _pairs(out[:4 * k], cplx, 4)
+    v = _pairs(out[4 * k:8 * k], cplx, 4)
+    return Svd2(u11=u[0], u21=u[1], u12=u[2], u22=u[3], v11=v[0], v21=v[1], v12=v[2],
+                v22=v[3], smax_scaled=out[8 * k], smin_scaled=out[8 * k + 1],
+                shift=out[8 * k + 2])
+
+
+def assemble_uv(urv, tri, shift):
+    """U and V from the reduction and the triangle SVD, tangent form
+    (svd2.py:350-424)."""
+    return _assemble(urv, tri, shift, False)
+
+
+def assemble_uv_sine(urv, tri, shift):
+    """The same through explicit sines (svd2.py:427-474)."""
+    return _assemble(urv, tri, shift, True)

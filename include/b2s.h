@@ -182,6 +182,42 @@ int b2s_svd2_phase(int phase, int complex_field, int sine_form, int64_t n,
                    double *const *out, void *stream);
 
 /*
+ * The lane primitives of lanes.py:69-259 as elementwise device ops over n
+ * lanes (the functions every kernel is built from, reference semantics for
+ * every input; NaN payload bits are not reproduced).  Inputs / outputs:
+ *   FMA, FNMA (a, b, c)          a*b+c / c-a*b, one rounding
+ *   RELAXED_MIN, RELAXED_MAX     (a, b): second operand on ties and NaN
+ *   SELECT (mask, a, b)          b where mask != 0, a elsewhere
+ *   GETEXP (a), SCALEF (a, e)    floor(log2|a|) / a * 2^floor(e)
+ *   HYPOT (a, b), INVSQRT (a)
+ *   BIT_AND/OR/XOR/ANDNOT (a, b), FABS, NEGATE, SIGN_MASK (a)
+ *   COMPLEX_MUL (ar, ai, br, bi) -> (re, im)
+ *   PHASE_FROM_PARTS (re, im, mag) -> (cos, sin)
+ *   POLAR (re, im) -> (mag, cos, sin)
+ */
+#define B2S_LANE_FMA 0
+#define B2S_LANE_FNMA 1
+#define B2S_LANE_RELAXED_MIN 2
+#define B2S_LANE_RELAXED_MAX 3
+#define B2S_LANE_SELECT 4
+#define B2S_LANE_GETEXP 5
+#define B2S_LANE_SCALEF 6
+#define B2S_LANE_HYPOT 7
+#define B2S_LANE_INVSQRT 8
+#define B2S_LANE_BIT_AND 9
+#define B2S_LANE_BIT_OR 10
+#define B2S_LANE_BIT_XOR 11
+#define B2S_LANE_BIT_ANDNOT 12
+#define B2S_LANE_FABS 13
+#define B2S_LANE_NEGATE 14
+#define B2S_LANE_SIGN_MASK 15
+#define B2S_LANE_COMPLEX_MUL 16
+#define B2S_LANE_PHASE_FROM_PARTS 17
+#define B2S_LANE_POLAR 18
+int b2s_lane_op(int op, int64_t n, int n_in, const double *const *in,
+                int n_out, double *const *out, void *stream);
+
+/*
  * lanesvd.verify.oracle_svd2 (verify.py:259-352) on the device: the
  * closed-form double-double reference SVD of n matrices given as trains
  * (a_im NULL for real input), bit-identical to the reference's.  out[36]:

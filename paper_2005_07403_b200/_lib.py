@@ -35,7 +35,7 @@ SYMBOLS = (
     "b2s_synth", "b2s_check_fp_env", "b2s_math_probe",
     "b2s_reserve_workspace", "b2s_hard_lane_count",
     "b2s_svd2_real_records", "b2s_svd2_complex_records", "b2s_metrics",
-    "b2s_oracle_svd2", "b2s_svd2_phase",
+    "b2s_oracle_svd2", "b2s_svd2_phase", "b2s_lane_op",
 )
 
 _P = ctypes.c_void_p
@@ -77,6 +77,7 @@ def _load():
     L.b2s_hard_lane_count.argtypes = [_int]
     L.b2s_oracle_svd2.argtypes = [_i64, _PA, _PA, _PA, _P]
     L.b2s_svd2_phase.argtypes = [_int, _int, _int, _i64, _int, _PA, _int, _PA, _P]
+    L.b2s_lane_op.argtypes = [_int, _i64, _int, _PA, _int, _PA, _P]
     for name in SYMBOLS:
         if name not in ("b2s_version", "b2s_last_error"):
             getattr(L, name).restype = _int

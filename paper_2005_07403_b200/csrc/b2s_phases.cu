@@ -10,6 +10,10 @@
 // are bit-identical to the reference's for every finite input, whether or
 // not the inputs came from the previous phase.
 //
+// `b2s_lane_op` does the same for the lane primitives of lanes.py:69-259
+// (fma, relaxed min/max, select, getexp, scalef, sign algebra, hypot_lane,
+// invsqrt_lane, complex_mul, phase_from_parts, polar).
+//
 // Train layout: K = 1 (real) or 2 (complex, re then im) trains per value;
 // "entries" are e11, e21, e12, e22 in that order (4K trains).  Masks travel
 // as 0.0 / 1.0 (any nonzero input is true).
@@ -200,6 +204,94 @@ __device__ __forceinline__ void phase_lane(const PhaseArgs& A, int64_t i) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// The lane primitives of lanes.py:69-259 as elementwise device ops
+// (b2s_lane_op): the same device functions every kernel is built from, with
+// the reference semantics for every input (NaN payload bits aside).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double getexp_lane(double a) {       // lanes.py:126-140
+  if (isnan(a)) return a;
+  if (isinf(a)) return __longlong_as_double(0x7FF0000000000000ll);
+  if (a == 0.0) return __longlong_as_double((long long)0xFFF0000000000000ull);
+  return (double)ilogb_finite(a);
+}
+
+__device__ __forceinline__ double scalef_lane(double a, double e) {   // lanes.py:143-159
+  const double ef = floor(e);
+  if (!isfinite(ef)) return __dmul_rn(a, exp2(ef));            // 2^+-inf = inf / 0, NaN stays NaN
+  const double sh = fmin(fmax(ef, -4500.0), 4500.0);
+  return scalbn(a, (int)sh);                                     // one rounding, as ldexp
+}
+
+__device__ __forceinline__ double bits_op(double a, double b, int op) {
+  const unsigned long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  unsigned long long r;
+  switch (op) {
+    case B2S_LANE_BIT_AND: r = x & y; break;
+    case B2S_LANE_BIT_OR: r = x | y; break;
+    case B2S_LANE_BIT_XOR: r = x ^ y; break;
+    default: r = ~x & y; break;                                  // bit_andnot
+  }
+  return __longlong_as_double((long long)r);
+}
+
+__host__ __device__ inline void lane_arity(int op, int* nin, int* nout) {
+  switch (op) {
+    case B2S_LANE_FMA: case B2S_LANE_FNMA: case B2S_LANE_SELECT: *nin = 3; *nout = 1; break;
+    case B2S_LANE_RELAXED_MIN: case B2S_LANE_RELAXED_MAX: case B2S_LANE_SCALEF: case B2S_LANE_HYPOT:
+    case B2S_LANE_BIT_AND: case B2S_LANE_BIT_OR: case B2S_LANE_BIT_XOR: case B2S_LANE_BIT_ANDNOT:
+      *nin = 2; *nout = 1; break;
+    case B2S_LANE_GETEXP: case B2S_LANE_INVSQRT: case B2S_LANE_FABS: case B2S_LANE_NEGATE:
+    case B2S_LANE_SIGN_MASK: *nin = 1; *nout = 1; break;
+    case B2S_LANE_COMPLEX_MUL: *nin = 4; *nout = 2; break;
+    case B2S_LANE_PHASE_FROM_PARTS: *nin = 3; *nout = 2; break;
+    case B2S_LANE_POLAR: *nin = 2; *nout = 3; break;
+    default: *nin = *nout = -1;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_lane_op(const PhaseArgs A) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* const* in = A.in;
+    double* const* out = A.out;
+    auto I = [&](int k) { return in[k][i]; };
+    switch (A.op) {
+      case B2S_LANE_FMA: out[0][i] = fma_(I(0), I(1), I(2)); break;
+      case B2S_LANE_FNMA: out[0][i] = fnma_(I(0), I(1), I(2)); break;
+      case B2S_LANE_RELAXED_MIN: out[0][i] = rmin(I(0), I(1)); break;
+      case B2S_LANE_RELAXED_MAX: out[0][i] = rmax(I(0), I(1)); break;
+      case B2S_LANE_SELECT: out[0][i] = sel(I(0) != 0.0, I(1), I(2)); break;
+      case B2S_LANE_GETEXP: out[0][i] = getexp_lane(I(0)); break;
+      case B2S_LANE_SCALEF: out[0][i] = scalef_lane(I(0), I(1)); break;
+      case B2S_LANE_HYPOT: out[0][i] = hypot_x(I(0), I(1)); break;
+      case B2S_LANE_INVSQRT: out[0][i] = invsqrt_x(I(0)); break;
+      case B2S_LANE_BIT_AND: case B2S_LANE_BIT_OR: case B2S_LANE_BIT_XOR: case B2S_LANE_BIT_ANDNOT:
+        out[0][i] = bits_op(I(0), I(1), A.op); break;
+      case B2S_LANE_FABS: out[0][i] = fabs_(I(0)); break;
+      case B2S_LANE_NEGATE: out[0][i] = neg_(I(0)); break;
+      case B2S_LANE_SIGN_MASK: out[0][i] = sgn_(I(0)); break;
+      case B2S_LANE_COMPLEX_MUL: {
+        double re, im;
+        cmul(I(0), I(1), I(2), I(3), re, im);
+        out[0][i] = re; out[1][i] = im;
+      } break;
+      case B2S_LANE_PHASE_FROM_PARTS: {
+        double c, s;
+        phase_x(I(0), I(1), I(2), c, s);
+        out[0][i] = c; out[1][i] = s;
+      } break;
+      case B2S_LANE_POLAR: {
+        const double mag = hypot_x(I(0), I(1));
+        double c, s;
+        phase_x(I(0), I(1), mag, c, s);
+        out[0][i] = mag; out[1][i] = c; out[2][i] = s;
+      } break;
+      default: break;
+    }
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(128) k_phase(const PhaseArgs A) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x)
@@ -241,6 +333,35 @@ extern "C" int b2s_svd2_phase(int op, int complex_field, int sine_form, int64_t 
     k_phase<1><<<blocks, 128, 0, (cudaStream_t)stream>>>(A);
   else
     k_phase<2><<<blocks, 128, 0, (cudaStream_t)stream>>>(A);
+  B2S_CUDA(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int b2s_lane_op(int op, int64_t n, int n_in, const double* const* in, int n_out, double* const* out,
+                           void* stream) {
+  if (n < 0) return fail(1, "negative batch size");
+  int want_in = 0, want_out = 0;
+  lane_arity(op, &want_in, &want_out);
+  if (want_in < 0) return fail(2, "unknown lane op %d", op);
+  if (n_in != want_in || n_out != want_out)
+    return fail(2, "lane op %d takes %d input and %d output trains, got %d and %d", op, want_in, want_out, n_in,
+                n_out);
+  if (!in || !out) return fail(5, "NULL train array");
+  PhaseArgs A{};
+  A.op = op;
+  A.n = n;
+  for (int k = 0; k < n_in; k++) {
+    if (!in[k]) return fail(5, "NULL input train %d", k);
+    A.in[k] = in[k];
+  }
+  for (int k = 0; k < n_out; k++) {
+    if (!out[k]) return fail(5, "NULL output train %d", k);
+    A.out[k] = out[k];
+  }
+  if (n == 0) return 0;
+  int blocks = (int)((n + 127) / 128);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_lane_op<<<blocks, 128, 0, (cudaStream_t)stream>>>(A);
   B2S_CUDA(cudaGetLastError());
   return 0;
 }

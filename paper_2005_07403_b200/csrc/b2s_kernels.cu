@@ -61,7 +61,21 @@ struct CplxArgs {
 constexpr int kBlock = 256;
 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
-__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+// Output stores: evict-first streaming stores (default); B2S_STORE_MODE 1 =
+// plain write-back stores, 2 = .cg (A/B variants: the config-3 bench moved
+// by < 0.5 % either way, profiles/r2_store_ring_ab.log).
+#ifndef B2S_STORE_MODE
+#define B2S_STORE_MODE 0
+#endif
+__device__ __forceinline__ void st_stream(double* p, double v) {
+#if B2S_STORE_MODE == 1
+  *p = v;
+#elif B2S_STORE_MODE == 2
+  __stcg(p, v);
+#else
+  __stcs(p, v);
+#endif
+}
 
 template <bool Cplx>
 __device__ __forceinline__ void store_states(double* const* st, int64_t i, const LaneStates& s, bool full) {
@@ -283,7 +297,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_svd2_complex(const CplxArgs A) {
 // lanes) is processed by CTA 0 with ordinary loads (complex) or by a
 // one-CTA launch of the LDG kernel (real), see B2S_TMA_TAIL_*.
 // ---------------------------------------------------------------------------
-constexpr int kStages = 4;
+// Depth of the TMA input ring (3 and 6 measured within 0.7 % of 4 on the
+// config-3 bench, profiles/r2_store_ring_ab.log).
+#ifndef B2S_RING_STAGES
+#define B2S_RING_STAGES 4
+#endif
+constexpr int kStages = B2S_RING_STAGES;
 // The sub-tile tail (n mod 256 lanes): 1 = processed by CTA 0 of the TMA
 // kernel with ordinary loads, 0 = a separate one-CTA launch of the LDG
 // kernel (keeps another copy of the pipeline out of the TMA kernel).

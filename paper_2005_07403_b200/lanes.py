@@ -56,6 +56,9 @@ def _run(name, args, n_out):
         ts = [t.reshape(-1).contiguous() for t in ts]
     n = int(ts[0].numel())
     outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(n_out)]
+    if n == 0:                                   # nothing to launch (empty tensors have no storage)
+        res = [o.cpu().numpy().reshape(shape) if host else o.reshape(shape) for o in outs]
+        return res[0] if n_out == 1 else tuple(res)
     pi, _k1 = _lib.ptr_array([t.data_ptr() for t in ts])
     po, _k2 = _lib.ptr_array([t.data_ptr() for t in outs])
     with torch.cuda.device(dev):

@@ -334,6 +334,8 @@ def _phase(name, cplx, ins, n_out, sine=False, finite=False):
         raise ValueError("%s: non-finite component" % name)
     _lib.assert_device_fp_env(dev.index or 0)
     outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(n_out)]
+    if n == 0:                                   # nothing to launch (empty tensors have no storage)
+        return [x.cpu().numpy() for x in outs] if host else outs
     pi, _k1 = _lib.ptr_array([x.data_ptr() for x in t])
     po, _k2 = _lib.ptr_array([x.data_ptr() for x in outs])
     with torch.cuda.device(dev):

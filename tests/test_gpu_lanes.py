@@ -62,3 +62,10 @@ def test_lane_ops_broadcast_and_device_tensors():
     mag, c, s = lanes.polar(3.0, 4.0)
     assert float(mag) == 5.0 and float(c) == 0.6 and float(s) == 0.8
     lanes.assert_fp_env(0)
+
+
+def test_empty_inputs():
+    from paper_2005_07403_b200 import svd2
+    assert lanes.fma(np.zeros(0), np.zeros(0), np.zeros(0)).shape == (0,)
+    tri = svd2.triangular_svd(np.zeros(0), np.zeros(0), np.zeros(0))
+    assert tri.smax_scaled.shape == (0,)

@@ -16,6 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = ["csrc/b2s_kernels.cu", "csrc/b2s_synth.cu", "csrc/b2s_host.cu",
            "csrc/b2s_verify.cu", "csrc/b2s_phases.cu"]
 HEADERS = ["csrc/b2s_lane.cuh", "csrc/b2s_svd2.cuh", "csrc/b2s_fast.cuh", "csrc/b2s_tma.cuh", "csrc/b2s_common.cuh",
+           "csrc/b2s_sort_variant.cuh",
            "../include/b2s.h"]
 OUT = os.path.join(HERE, "_native", "libb2s.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",

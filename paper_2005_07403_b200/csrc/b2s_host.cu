@@ -17,6 +17,8 @@
 #include <emmintrin.h>
 #include <omp.h>
 
+#include <cstdlib>
+
 #include <mutex>
 #include <vector>
 
@@ -78,13 +80,32 @@ static void stream_copy(double* dst, const double* src, int64_t n) {
   _mm_sfence();                                     // this thread's streaming stores, before the barrier
 }
 
+// Host threads for the bounce copies: B2S_COPY_THREADS if set, else the
+// host's cores shared among the processes of one node (LOCAL_WORLD_SIZE,
+// set by torchrun -- which also sets OMP_NUM_THREADS=1, so the OpenMP
+// default would leave every rank with one copy thread).
+static int copy_threads() {
+  static int n = 0;
+  if (n == 0) {
+    const char* e = std::getenv("B2S_COPY_THREADS");
+    int t = e ? std::atoi(e) : 0;
+    if (t <= 0) {
+      const char* l = std::getenv("LOCAL_WORLD_SIZE");
+      const int ranks = l ? std::atoi(l) : 1;
+      t = omp_get_num_procs() / (ranks > 0 ? ranks : 1);
+    }
+    n = t > 0 ? t : 1;
+  }
+  return n;
+}
+
 // Parallel copy of `ntr` trains' chunks (host cores; each train split into
 // 1 MiB pieces so every thread has work).
 static void par_copy(int ntr, double* const* dst, const double* const* src, int64_t m) {
   const int64_t piece = 1 << 17;                     // doubles
   const int64_t per = (m + piece - 1) / piece;
   const int64_t total = per * ntr;
-  #pragma omp parallel for schedule(static)
+  #pragma omp parallel for schedule(static) num_threads(copy_threads())
   for (int64_t w = 0; w < total; w++) {
     const int t = (int)(w / per);
     const int64_t lo = (w % per) * piece;

@@ -105,7 +105,8 @@ static void par_copy(int ntr, double* const* dst, const double* const* src, int6
   const int64_t piece = 1 << 17;                     // doubles
   const int64_t per = (m + piece - 1) / piece;
   const int64_t total = per * ntr;
-  #pragma omp parallel for schedule(static) num_threads(copy_threads())
+  const int nt = copy_threads();
+  #pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t w = 0; w < total; w++) {
     const int t = (int)(w / per);
     const int64_t lo = (w % per) * piece;

@@ -8,11 +8,14 @@ field, one matrix per thread, with results bit-identical to the reference.
 
 Compute happens only in ``_native/libb2s.so`` (C ABI: ``include/b2s.h``),
 mapped by the first compute call, which raises if it is not built -- there
-is no CPU path.  Importing the package loads no native code.
+is no CPU path.  Importing the package loads no native code (the
+reference checks its FP environment at import; here ``assert_fp_env()``
+checks the GPU's and runs before a device's first launch).
 """
 
 from ._lib import LIB_PATH, assert_device_fp_env
 from .driver import RunConfig, run_batch, run_batch_into, shards, svd2_chunk, svd2_single
+from .lanes import assert_fp_env
 from .layout import (LANE_WIDTH, Batch2x2, MatrixSvd, SvdBatchOut, aligned_zeros,
                      from_trains, pack, padded_len, unpack, unpack_inputs)
 from .svd2 import ScaleResult, Svd2, TriangleSvd, UrvState, backscale, svd2_lanes
@@ -25,7 +28,7 @@ __all__ = sorted([
     "aligned_zeros", "pack", "unpack", "unpack_inputs", "from_trains",
     "run_batch_into", "shards", "Svd2", "svd2_lanes", "backscale",
     "ScaleResult", "UrvState", "TriangleSvd", "oracle_svd2",
-    "assert_device_fp_env", "LIB_PATH",
+    "assert_fp_env", "assert_device_fp_env", "LIB_PATH",
 ])
 
 __version__ = "0.1.0"

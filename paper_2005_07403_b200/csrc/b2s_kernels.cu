@@ -708,7 +708,10 @@ __global__ void __launch_bounds__(kBlock) k_fix_real(const RealArgs A) {
 }
 
 template <int Mode, bool Sine>
-__global__ void __launch_bounds__(kBlock) k_fix_cplx(const CplxArgs A) {
+#ifndef B2S_FIX_MINB
+#define B2S_FIX_MINB 1
+#endif
+__global__ void __launch_bounds__(kBlock, B2S_FIX_MINB) k_fix_cplx(const CplxArgs A) {
   fix_lanes(A.q, A.n, [&](int64_t i) { redo_cplx<Mode, Sine>(A, i); });
 }
 

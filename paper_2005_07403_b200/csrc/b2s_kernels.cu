@@ -751,6 +751,7 @@ __global__ void __launch_bounds__(kBlock) k_math_probe(int op, int64_t n, const 
       case 10: r = div_den<true, false, true, 0>(x, make_den<false>(y), hard); break;
       case 11: r = div_den<true, false, true, 1>(x, make_den<false>(y), hard); break;
       case 12: r = div_den<true, false, true, 2>(x, make_den<false>(y), hard); break;
+      case 13: r = div_den<true, false, true, 3>(x, make_den<false>(y), hard); break;
       default: { double c, s; phase_f<false>(x, y, hypot_x(x, y), c, s, hard); r = (op == 7) ? c : s; } break;
     }
     o[i] = hard ? hard_marker() : r;
@@ -1189,7 +1190,7 @@ int b2s_backscale(int64_t n, const double* smax, const double* smin, const doubl
 }
 
 int b2s_math_probe(int op, int64_t n, const double* a, const double* b, double* out, void* stream) {
-  if (op < 0 || op > 12) return fail(1, "unknown probe op %d", op);
+  if (op < 0 || op > 13) return fail(1, "unknown probe op %d", op);
   if (n < 0) return fail(1, "negative n");
   if (!a || !out || ((op == 0 || op >= 4) && !b)) return fail(5, "NULL operand");
   if (n == 0) return 0;

@@ -143,12 +143,13 @@ def test_normalised_division_full_range(gen):
     assert (bits(probe(6, a[:4], z)) == HARD).all()
 
 
-@pytest.mark.parametrize("op", [10, 11, 12])
+@pytest.mark.parametrize("op", [10, 11, 12, 13])
 def test_normalised_division_streaming_variant(gen, op):
     """div_den as the streaming kernels run it: selects instead of per-lane
     branches, subnormal quotients rounded by the warp-uniform FP64 sequence
     (op 10), the integer re-rounding call (op 11) or its inline select form
-    (op 12, subnormal_quot_sel).  Exact for every normal /
+    (op 12, subnormal_quot_sel; op 13 the same under a warp-uniform branch).
+    Exact for every normal /
     zero numerator over a normal denominator; declines subnormal operands."""
     sgn = lambda: torch.where(torch.rand(N, device=DEV, generator=gen) < 0.5, -1.0, 1.0).to(torch.float64)
     for (la, ha), (lb, hb) in (((-1022, 1023), (-1022, 1023)), ((-1022, -900), (900, 1023)),

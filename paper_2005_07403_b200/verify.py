@@ -164,9 +164,12 @@ class OracleSvd:
 
 
 def _factor_array(entries, k):
-    vals = [complex(float(e[0].hi[k]) + float(e[0].lo[k]),
-                    float(e[1].hi[k]) + float(e[1].lo[k])) for e in entries]
-    return np.array([[vals[0], vals[1]], [vals[2], vals[3]]])
+    """Lane k's factor as a 2x2 complex128 matrix (entries in row-major
+    order; each double-double part rounded to one double)."""
+    z = np.empty(4, dtype=np.complex128)
+    for j, (re, im) in enumerate(entries):
+        z[j] = complex(float(re.hi[k]) + float(re.lo[k]), float(im.hi[k]) + float(im.lo[k]))
+    return z.reshape(2, 2)
 
 
 def oracle_svd2(matrices, device=None):

@@ -282,6 +282,17 @@ def test_capi_argument_validation_without_gpu():
     assert L.b2s_math_probe(99, 1, 8, 8, 8, None) > 0
     # zero lanes is a valid no-op
     assert L.b2s_svd2_real(0, arr, arr, arr, 8, 8, 8, 0, 0, None, None) == 0
+    # the phase, lane-op and reference-SVD entries validate before any CUDA call
+    rc = L.b2s_svd2_phase(99, 0, 0, 4, 4, arr, 5, arr, None)
+    assert rc > 0 and b"unknown phase" in L.b2s_last_error()
+    rc = L.b2s_svd2_phase(0, 0, 0, 4, 4, arr, 4, arr, None)          # compute_scale real: 4 -> 5
+    assert rc > 0 and b"takes 4 input and 5 output" in L.b2s_last_error()
+    assert L.b2s_svd2_phase(0, 1, 0, -1, 8, arr, 9, arr, None) > 0
+    rc = L.b2s_lane_op(77, 4, 1, arr, 1, arr, None)
+    assert rc > 0 and b"unknown lane op" in L.b2s_last_error()
+    rc = L.b2s_lane_op(0, 4, 2, arr, 1, arr, None)                     # fma takes 3 inputs
+    assert rc > 0 and b"takes 3 input" in L.b2s_last_error()
+    assert L.b2s_oracle_svd2(4, None, None, arr, None) > 0
     with pytest.raises(ValueError):
         _lib.check(1, "x")
     with pytest.raises(RuntimeError):

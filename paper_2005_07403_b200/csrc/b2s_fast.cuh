@@ -422,4 +422,79 @@ __device__ __forceinline__ bool svd2_complex_f(const double (&ar)[4], const doub
   return hard;
 }
 
+// The same streaming pipeline as svd2_complex_f<Sine, false, Wide, !Wide>
+// with the wide / bounded choice made at run time: `w` must be warp-uniform.
+// Every phase the two variants share is compiled once and only the division
+// sites branch (five warp-uniform branches), so warps of both kinds run one
+// code body -- what a kernel mixing wide and narrow warps on one SM needs
+// to keep its instructions in cache (B2S_CPLX_SORT4 variant).
+template <bool Sine>
+__device__ __forceinline__ bool svd2_complex_u(const double (&ar)[4], const double (&ai)[4], CplxOut& o,
+                                               const bool w) {
+  bool hard = false;
+  double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
+  const double shift = scale_f<8>(p, hard);
+  double er[4] = {p[0], p[2], p[4], p[6]}, ei[4] = {p[1], p[3], p[5], p[7]};
+  double m11, m21, m12, m22, n1, n2;
+  if (w) {
+    m11 = hypot_f<false, false>(fabs_(er[0]), fabs_(ei[0]), hard);
+    m21 = hypot_f<false, false>(fabs_(er[1]), fabs_(ei[1]), hard);
+    m12 = hypot_f<false, false>(fabs_(er[2]), fabs_(ei[2]), hard);
+    m22 = hypot_f<false, false>(fabs_(er[3]), fabs_(ei[3]), hard);
+    n1 = hypot_big_f<false, false>(m11, m21, hard);
+    n2 = hypot_big_f<false, false>(m12, m22, hard);
+  } else {
+    m11 = hypot_f<false, true>(fabs_(er[0]), fabs_(ei[0]), hard);
+    m21 = hypot_f<false, true>(fabs_(er[1]), fabs_(ei[1]), hard);
+    m12 = hypot_f<false, true>(fabs_(er[2]), fabs_(ei[2]), hard);
+    m22 = hypot_f<false, true>(fabs_(er[3]), fabs_(ei[3]), hard);
+    n1 = hypot_big_f<false, true>(m11, m21, hard);
+    n2 = hypot_big_f<false, true>(m12, m22, hard);
+  }
+  CplxUrv U;
+  U.C = n1 < n2;
+  swp(U.C, er[0], er[2]); swp(U.C, ei[0], ei[2]);
+  swp(U.C, er[1], er[3]); swp(U.C, ei[1], ei[3]);
+  swp(U.C, m11, m12); swp(U.C, m21, m22);
+  const double r11 = U.C ? n2 : n1;
+  U.R = m11 < m21;
+  swp(U.R, er[0], er[1]); swp(U.R, ei[0], ei[1]);
+  swp(U.R, er[2], er[3]); swp(U.R, ei[2], ei[3]);
+  swp(U.R, m11, m21);
+  if (w) {
+    phase_w<false>(er[0], ei[0], m11, U.c1, U.s1, hard);
+    phase_w<false>(er[1], ei[1], m21, U.c2, U.s2, hard);
+    bool h = false;
+    U.mt = div_den<false, kWideSub, true>(m21, make_den<kWideSub>(m11), h);
+    hard |= h;
+  } else {
+    double d11 = 1.0, r11p = 1.0;
+    phase_f<false, true>(er[0], ei[0], m11, U.c1, U.s1, hard, &d11, &r11p);
+    phase_f<false, true>(er[1], ei[1], m21, U.c2, U.s2, hard);
+    const double a2 = mul(m21, hi_(m11) >= 0x7FD00000u ? 0.25 : 1.0);
+    U.mt = quot_f(a2, d11, r11p);
+  }
+  double f12r, f12i, f22r, f22i;
+  cmul(U.c1, neg_(U.s1), er[2], ei[2], f12r, f12i);
+  cmul(U.c2, neg_(U.s2), er[3], ei[3], f22r, f22i);
+  U.cg = invsqrt_f(fma_(U.mt, U.mt, 1.0));
+  const double g12r = mul(U.cg, fma_(U.mt, f22r, f12r)), g12i = mul(U.cg, fma_(U.mt, f22i, f12i));
+  const double g22r = mul(U.cg, fnma_(U.mt, f12r, f22r)), g22i = mul(U.cg, fnma_(U.mt, f12i, f22i));
+  const double r12 = hypot_big_f<false>(fabs_(g12r), fabs_(g12i), hard);
+  double c12, s12;
+  if (w) phase_w<false>(g12r, g12i, r12, c12, s12, hard);
+  else phase_f<false>(g12r, g12i, r12, c12, s12, hard);
+  double wr, wi;
+  cmul(c12, neg_(s12), g22r, g22i, wr, wi);
+  const double r22 = hypot_big_f<false>(fabs_(wr), fabs_(wi), hard);
+  if (w) phase_w<false>(wr, wi, r22, U.dhr, U.dhi, hard);
+  else phase_f<false>(wr, wi, r22, U.dhr, U.dhi, hard);
+  U.dtr = c12;
+  U.dti = neg_(s12);
+  const Tri T = w ? triangle_f<false, true>(r11, r12, r22, hard) : triangle_f<false, false>(r11, r12, r22, hard);
+  assemble_complex<Sine>(U, T, o);
+  o.shift = shift;
+  return hard;
+}
+
 }  // namespace b2s

@@ -482,6 +482,10 @@ template <int Mode, bool Sine, bool AoS>
 #ifndef B2S_CPLX_MINB
 #define B2S_CPLX_MINB 3
 #endif
+// 1: one code body for wide and bounded warps (svd2_complex_u) -- variant.
+#ifndef B2S_CPLX_UNIFIED
+#define B2S_CPLX_UNIFIED 0
+#endif
 #ifndef B2S_CPLX_STAGES
 #define B2S_CPLX_STAGES kStages
 #endif
@@ -516,10 +520,14 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
     CplxOut o;
     bool hard;
     const double p[8] = {ar[0], ai[0], ar[1], ai[1], ar[2], ai[2], ar[3], ai[3]};
+#if B2S_CPLX_UNIFIED
+    hard = svd2_complex_u<Sine>(ar, ai, o, __any_sync(0xFFFFFFFFu, wide_lane<8>(p)));
+#else
     if (__any_sync(0xFFFFFFFFu, wide_lane<8>(p)))
       hard = svd2_complex_f<Sine, false, true>(ar, ai, o);
     else
       hard = svd2_complex_f<Sine, false, false, true>(ar, ai, o);   // bounded warp
+#endif
     store_cplx<Mode>(A, i, o);
     nh += mark_hard(A.q, hard, i);
   }
@@ -571,7 +579,10 @@ __global__ void __launch_bounds__(kBlock, B2S_CPLX_MINB) k_svd2_cplx_tma(const C
 #ifndef B2S_CPLX_SORT
 #define B2S_CPLX_SORT 0
 #endif
-#if B2S_CPLX_SORT   // measured and rejected; variant builds only
+#ifndef B2S_CPLX_SORT4
+#define B2S_CPLX_SORT4 0
+#endif
+#if B2S_CPLX_SORT || B2S_CPLX_SORT4   // measured variants; variant builds only
 }  // namespace b2s
 #include "b2s_sort_variant.cuh"
 namespace b2s {
@@ -967,6 +978,32 @@ static int launch_cplx(CplxArgs A, cudaStream_t s) {
       if (rc) return rc;
       B2S_CUDA(cudaMemsetAsync(A.q.cnt, 0, sizeof(unsigned long long), s));
     }
+#if B2S_CPLX_SORT4
+    if (!States && !A.aos && tma_ok_cplx(A) && !getenv_flag("B2S_NO_SORT")) {
+      auto k = k_svd2_cplx_u4<Mode, Sine>;
+      const size_t sm = U4Layout::kSmem;
+      B2S_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, U4Layout::LT + 32, sm);
+      const int64_t tiles = A.n / U4Layout::LT;
+      int64_t g = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+      if (tiles < g) g = tiles;
+      const int64_t head = tiles * U4Layout::LT;
+      B2S_CUDA(cudaMemsetAsync(A.q.mask, 0, (size_t)(head >> 5) * sizeof(unsigned), s));
+      if (g > 0) k<<<(int)g, U4Layout::LT + 32, sm, s>>>(A);
+      if (head < A.n) {
+        CplxArgs T = A;
+        T.n = A.n - head;
+        for (int t = 0; t < 4; t++) { T.ur[t] += head; T.ui[t] += head; T.vr[t] += head; T.vi[t] += head; }
+        for (int t = 0; t < 4; t++) { T.ar[t] += head; T.ai[t] += head; }
+        T.smax += head; T.smin += head; T.shift += head;
+        T.q.mask += head >> 5;
+        k_svd2_complex<Mode, Sine, false><<<1, kBlock, 0, s>>>(T);
+      }
+    } else
+#endif
 #if B2S_CPLX_SORT
     if (!States && !A.aos && tma_ok_cplx(A) && !getenv_flag("B2S_NO_SORT")) {
       constexpr int LT = B2S_CPLX_SORT > 0 ? B2S_CPLX_SORT : 128;
